@@ -1,0 +1,706 @@
+// libsas.so — C ABI of the B200-native SubApSnap online phase (include/sas.h).
+//
+// One plan per (operator, basis X, selector S) on one CUDA device; it owns all
+// device memory.  sas_solve enqueues the per-parameter pipeline on the caller's
+// stream: [K3 Gaussian-row contraction] -> K4 batched least squares with a fused
+// assembly prologue (K1 affine / K2 stencil / precomputed M).  No CPU fallback:
+// every numerical step of the online path runs in the kernels below.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "../../include/sas.h"
+#include "sas_common.cuh"
+#include "k_lsq.cuh"
+#include "k_gauss.cuh"
+#include "k_recon.cuh"
+
+static const double h_exp2_tab64[64] = {
+    0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
+    0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0,
+    0x1.172b83c7d517bp+0, 0x1.1a35beb6fcb75p+0, 0x1.1d4873168b9aap+0, 0x1.2063b88628cd6p+0,
+    0x1.2387a6e756238p+0, 0x1.26b4565e27cddp+0, 0x1.29e9df51fdee1p+0, 0x1.2d285a6e4030bp+0,
+    0x1.306fe0a31b715p+0, 0x1.33c08b26416ffp+0, 0x1.371a7373aa9cbp+0, 0x1.3a7db34e59ff7p+0,
+    0x1.3dea64c123422p+0, 0x1.4160a21f72e2ap+0, 0x1.44e086061892dp+0, 0x1.486a2b5c13cd0p+0,
+    0x1.4bfdad5362a27p+0, 0x1.4f9b2769d2ca7p+0, 0x1.5342b569d4f82p+0, 0x1.56f4736b527dap+0,
+    0x1.5ab07dd485429p+0, 0x1.5e76f15ad2148p+0, 0x1.6247eb03a5585p+0, 0x1.6623882552225p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.6dfb23c651a2fp+0, 0x1.71f75e8ec5f74p+0, 0x1.75feb564267c9p+0,
+    0x1.7a11473eb0187p+0, 0x1.7e2f336cf4e62p+0, 0x1.82589994cce13p+0, 0x1.868d99b4492edp+0,
+    0x1.8ace5422aa0dbp+0, 0x1.8f1ae99157736p+0, 0x1.93737b0cdc5e5p+0, 0x1.97d829fde4e50p+0,
+    0x1.9c49182a3f090p+0, 0x1.a0c667b5de565p+0, 0x1.a5503b23e255dp+0, 0x1.a9e6b5579fdbfp+0,
+    0x1.ae89f995ad3adp+0, 0x1.b33a2b84f15fbp+0, 0x1.b7f76f2fb5e47p+0, 0x1.bcc1e904bc1d2p+0,
+    0x1.c199bdd85529cp+0, 0x1.c67f12e57d14bp+0, 0x1.cb720dcef9069p+0, 0x1.d072d4a07897cp+0,
+    0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
+    0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0};
+
+// ---------------------------------------------------------------------------
+// errors
+static thread_local std::string g_err;
+void sas_set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+#define ARG_CHECK(cond, ...)        \
+  do {                              \
+    if (!(cond)) {                  \
+      sas_set_error(__VA_ARGS__);   \
+      return SAS_ERR_ARG;           \
+    }                               \
+  } while (0)
+
+double sas_exp64_host(double x) {
+  volatile double kd = fma(x, SAS_INVLN2X64, SAS_EXP_MAGIC);
+  int64_t bits;
+  double kdv = kd;
+  memcpy(&bits, &kdv, 8);
+  int ki = (int)(uint32_t)(bits & 0xffffffffu);
+  double kf = kdv - SAS_EXP_MAGIC;
+  double r = fma(-kf, SAS_LN2D64_HI, x);
+  r = fma(-kf, SAS_LN2D64_LO, r);
+  double q = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+  q = fma(q, r, 1.0 / 6.0);
+  q = fma(q, r, 0.5);
+  q = fma(q, r, 1.0);
+  q = q * r;
+  double t = h_exp2_tab64[ki & 63];
+  double res = fma(t, q, t);
+  int e = ki >> 6;
+  int64_t rb;
+  memcpy(&rb, &res, 8);
+  rb += (int64_t)e << 52;
+  memcpy(&res, &rb, 8);
+  return (x < -708.39) ? 0.0 : res;
+}
+
+// ---------------------------------------------------------------------------
+struct sas_plan {
+  int device = 0;
+  int op = 0, dtype = 0, dp = 1, pcomplex = 0;
+  int64_t n = 0;
+  int r = 0, s = 0;
+  size_t esz = 8;  // element size of dtype
+  void* X = nullptr;
+  int64_t* S = nullptr;
+  double* w = nullptr;
+  void* t = nullptr;
+  void* proj = nullptr;
+  // affine
+  int K = 0;
+  int32_t* kind = nullptr;
+  double* scale = nullptr;
+  double* rate = nullptr;
+  void* blocks = nullptr;
+  std::vector<int32_t> h_kind;
+  // stencil
+  int E = 0;
+  double* phi = nullptr;
+  double* G = nullptr;
+  double hh = 1.0;
+  // gauss
+  double* pts = nullptr;
+  int pdim = 0;
+  double ridge = 0.0;
+  double* D = nullptr;
+  // full operator for the residual checker
+  int64_t* full_nbr = nullptr;
+  double* full_phi = nullptr;
+  void* full_b = nullptr;
+  std::vector<int64_t*> csr_rp, csr_ci;
+  std::vector<void*> csr_va;
+  int64_t** csr_rp_d = nullptr;
+  int64_t** csr_ci_d = nullptr;
+  void** csr_va_d = nullptr;
+  // scratch
+  double* Mscr = nullptr;
+  int64_t Mscr_P = 0;
+  double* rpart = nullptr;
+  int64_t rpart_n = 0;
+  void* fco = nullptr;
+  int64_t fco_n = 0;
+  // host-call staging
+  void* h_params = nullptr; int64_t h_params_n = 0;
+  void* h_ctab = nullptr; int64_t h_ctab_n = 0;
+  void* h_rhs = nullptr; int64_t h_rhs_n = 0;
+  void* h_coef = nullptr; int64_t h_coef_n = 0;
+  double* h_sres = nullptr; int64_t h_sres_n = 0;
+  double* h_outv = nullptr; int64_t h_outv_n = 0;
+  int32_t* h_status = nullptr; int64_t h_status_n = 0;
+  int32_t* h_bad = nullptr; int64_t h_bad_n = 0;
+  cudaStream_t stream = nullptr;
+  int32_t last_launches = 0;
+  int sms = 148;
+};
+
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DevGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+template <typename P>
+static int dalloc(P** ptr, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc((void**)ptr, bytes);
+  if (e != cudaSuccess) {
+    sas_set_error("cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+    return SAS_ERR_CUDA;
+  }
+  return SAS_OK;
+}
+
+template <typename P>
+static int dupload(P** ptr, const void* host, size_t bytes) {
+  int rc = dalloc(ptr, bytes);
+  if (rc) return rc;
+  if (host && bytes) SAS_CUDA_CHECK(cudaMemcpy(*ptr, host, bytes, cudaMemcpyHostToDevice));
+  return SAS_OK;
+}
+
+template <typename P>
+static int ensure(P** ptr, int64_t* have, int64_t need_bytes) {
+  if (*have >= need_bytes && *ptr) return SAS_OK;
+  if (*ptr) cudaFree(*ptr);
+  *ptr = nullptr;
+  *have = 0;
+  int rc = dalloc(ptr, (size_t)need_bytes);
+  if (rc) return rc;
+  *have = need_bytes;
+  return SAS_OK;
+}
+
+static void plan_free(sas_plan* pl) {
+  if (!pl) return;
+  DevGuard g(pl->device);
+  void* ptrs[] = {pl->X, pl->S, pl->w, pl->t, pl->proj, pl->kind, pl->scale, pl->rate, pl->blocks,
+                  pl->phi, pl->G, pl->pts, pl->D, pl->full_nbr, pl->full_phi, pl->full_b,
+                  pl->csr_rp_d, pl->csr_ci_d, pl->csr_va_d, pl->Mscr, pl->rpart, pl->fco,
+                  pl->h_params, pl->h_ctab, pl->h_rhs, pl->h_coef, pl->h_sres, pl->h_outv,
+                  pl->h_status, pl->h_bad};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (auto* p : pl->csr_rp) cudaFree(p);
+  for (auto* p : pl->csr_ci) cudaFree(p);
+  for (auto* p : pl->csr_va) cudaFree(p);
+  if (pl->stream) cudaStreamDestroy(pl->stream);
+  delete pl;
+}
+
+__global__ void k_stencil_gather(const double* __restrict__ X, int r, const int64_t* __restrict__ S,
+                                 const int64_t* __restrict__ nbr, int s, int E, double* __restrict__ G) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t tot = (int64_t)s * (E + 1) * r;
+  if (idx >= tot) return;
+  int j = (int)(idx % r);
+  int64_t ie = idx / r;
+  int e1 = (int)(ie % (E + 1));
+  int i = (int)(ie / (E + 1));
+  int64_t node = (e1 == 0) ? S[i] : nbr[(int64_t)i * E + e1 - 1];
+  G[idx] = (node >= 0) ? X[node * r + j] : 0.0;
+}
+
+extern "C" const char* sas_last_error(void) { return g_err.c_str(); }
+extern "C" const char* sas_version(void) { return "sas 0.1.0 (sm_100a)"; }
+extern "C" double sas_debug_exp64_host(double x) { return sas_exp64_host(x); }
+
+extern "C" int sas_plan_create(const sas_desc* desc, const void* X, int64_t n, int32_t r,
+                               const int64_t* S, const double* w, int32_t s, const void* t,
+                               const void* proj, int32_t device, uint32_t flags, sas_plan** out) {
+  ARG_CHECK(desc && out, "sas_plan_create: null desc/out");
+  ARG_CHECK(X && S && t, "sas_plan_create: X, S and t are required");
+  ARG_CHECK(n > 0 && r > 0 && s > 0, "sas_plan_create: bad sizes n=%lld r=%d s=%d", (long long)n, r, s);
+  ARG_CHECK(r <= 63, "sas_plan_create: r=%d exceeds the kernel limit 63", r);
+  ARG_CHECK(s >= r, "solve_ls requires rows >= cols (s=%d, r=%d)", s, r);
+  ARG_CHECK(s <= 512, "sas_plan_create: s=%d exceeds the kernel limit 512", s);
+  ARG_CHECK(desc->dtype == SAS_F64 || desc->dtype == SAS_C128, "sas_plan_create: bad dtype");
+  ARG_CHECK(desc->param_dim >= 1, "sas_plan_create: param_dim must be >= 1");
+  const int ndev_check = [] { int c = 0; cudaGetDeviceCount(&c); return c; }();
+  ARG_CHECK(device >= 0 && device < ndev_check, "sas_plan_create: device %d not available (%d devices)", device, ndev_check);
+  if (desc->dtype == SAS_C128) ARG_CHECK(r + 1 <= 64 && s <= 256, "complex plans need r <= 63, s <= 256");
+  if (r + 1 > 32) ARG_CHECK(s <= 256, "plans with r >= 32 need s <= 256");
+  if (desc->op_kind == SAS_OP_AFFINE) {
+    ARG_CHECK(desc->n_terms >= 1 && desc->n_terms <= 16, "affine: need 1..16 terms");
+    ARG_CHECK(desc->term_kind && desc->term_scale && desc->blocks, "affine: term_kind, term_scale and blocks are required");
+    for (int k = 0; k < desc->n_terms; ++k)
+      ARG_CHECK(desc->term_kind[k] >= 0 && desc->term_kind[k] <= 3, "affine: bad coefficient kind %d", desc->term_kind[k]);
+  } else if (desc->op_kind == SAS_OP_STENCIL) {
+    ARG_CHECK(desc->dtype == SAS_F64 && !desc->param_complex, "stencil: real f64 only");
+    ARG_CHECK(desc->n_edges >= 1 && desc->n_edges <= 8, "stencil: 1..8 edges per row");
+    ARG_CHECK(desc->edge_nbr && desc->edge_phi && desc->edge_div > 0, "stencil: edge_nbr, edge_phi, edge_div required");
+    for (int64_t q = 0; q < (int64_t)s * desc->n_edges; ++q)
+      ARG_CHECK(desc->edge_nbr[q] < n, "stencil: neighbour index out of range");
+  } else if (desc->op_kind == SAS_OP_GAUSS) {
+    ARG_CHECK(desc->dtype == SAS_F64 && !desc->param_complex && desc->param_dim == 1, "gauss: real scalar bandwidth only");
+    ARG_CHECK(desc->points && desc->point_dim >= 1, "gauss: points required");
+    ARG_CHECK(s <= 96, "gauss: s <= 96");
+  } else {
+    ARG_CHECK(false, "unknown op_kind %d", desc->op_kind);
+  }
+
+  sas_plan* pl = new sas_plan();
+  pl->device = device;
+  pl->op = desc->op_kind;
+  pl->dtype = desc->dtype;
+  pl->dp = desc->param_dim;
+  pl->pcomplex = desc->param_complex ? 1 : 0;
+  pl->n = n;
+  pl->r = r;
+  pl->s = s;
+  pl->esz = desc->dtype == SAS_C128 ? 16 : 8;
+  DevGuard g(device);
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, device);
+  pl->sms = prop.multiProcessorCount;
+  int rc = SAS_OK;
+#define TRY(x)                 \
+  do {                         \
+    rc = (x);                  \
+    if (rc) {                  \
+      plan_free(pl);           \
+      return rc;               \
+    }                          \
+  } while (0)
+  for (int i = 0; i < s; ++i) {
+    if (S[i] < 0 || S[i] >= n) {
+      plan_free(pl);
+      sas_set_error("selector index out of range for n=%lld", (long long)n);
+      return SAS_ERR_ARG;
+    }
+  }
+  if (w)
+    for (int i = 0; i < s; ++i)
+      if (!(w[i] > 0)) {
+        plan_free(pl);
+        sas_set_error("weights must be positive");
+        return SAS_ERR_ARG;
+      }
+  const size_t xbytes = (size_t)n * r * pl->esz;
+  if (flags & SAS_FLAG_INPUT_DEVICE) {
+    TRY(dalloc(&pl->X, xbytes));
+    cudaError_t e = cudaMemcpy(pl->X, X, xbytes, cudaMemcpyDeviceToDevice);
+    if (e != cudaSuccess) { plan_free(pl); sas_set_error("copy X: %s", cudaGetErrorString(e)); return SAS_ERR_CUDA; }
+  } else {
+    TRY(dupload(&pl->X, X, xbytes));
+  }
+  TRY(dupload(&pl->S, S, (size_t)s * sizeof(int64_t)));
+  if (w) TRY(dupload(&pl->w, w, (size_t)s * sizeof(double)));
+  TRY(dupload(&pl->t, t, (size_t)s * pl->esz));
+  if (proj) TRY(dupload(&pl->proj, proj, (size_t)r * pl->esz));
+
+  switch (desc->op_kind) {
+    case SAS_OP_AFFINE: {
+      pl->K = desc->n_terms;
+      pl->h_kind.assign(desc->term_kind, desc->term_kind + pl->K);
+      TRY(dupload(&pl->kind, desc->term_kind, pl->K * sizeof(int32_t)));
+      TRY(dupload(&pl->scale, desc->term_scale, pl->K * 2 * sizeof(double)));
+      std::vector<double> rate(2 * pl->K, 0.0);
+      if (desc->term_rate) memcpy(rate.data(), desc->term_rate, rate.size() * sizeof(double));
+      TRY(dupload(&pl->rate, rate.data(), rate.size() * sizeof(double)));
+      TRY(dupload(&pl->blocks, desc->blocks, (size_t)pl->K * s * r * pl->esz));
+      break;
+    }
+    case SAS_OP_STENCIL: {
+      pl->E = desc->n_edges;
+      pl->hh = desc->edge_div;
+      TRY(dupload(&pl->phi, desc->edge_phi, (size_t)s * pl->E * pl->dp * sizeof(double)));
+      int64_t* nbr_d = nullptr;
+      TRY(dupload(&nbr_d, desc->edge_nbr, (size_t)s * pl->E * sizeof(int64_t)));
+      rc = dalloc(&pl->G, (size_t)s * (pl->E + 1) * r * sizeof(double));
+      if (rc) { cudaFree(nbr_d); plan_free(pl); return rc; }
+      int64_t tot = (int64_t)s * (pl->E + 1) * r;
+      k_stencil_gather<<<(unsigned)((tot + 255) / 256), 256>>>((const double*)pl->X, r, pl->S, nbr_d, s, pl->E, pl->G);
+      cudaError_t e = cudaDeviceSynchronize();
+      cudaFree(nbr_d);
+      if (e != cudaSuccess) { plan_free(pl); sas_set_error("stencil gather: %s", cudaGetErrorString(e)); return SAS_ERR_CUDA; }
+      break;
+    }
+    case SAS_OP_GAUSS: {
+      pl->pdim = desc->point_dim;
+      pl->ridge = desc->ridge;
+      TRY(dupload(&pl->pts, desc->points, (size_t)n * pl->pdim * sizeof(double)));
+      TRY(dalloc(&pl->D, (size_t)s * n * sizeof(double)));
+      int64_t tot = (int64_t)s * n;
+      k_gauss_dist<<<(unsigned)((tot + 255) / 256), 256>>>(pl->pts, pl->S, n, pl->pdim, s, pl->D);
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) { plan_free(pl); sas_set_error("gauss dist: %s", cudaGetErrorString(e)); return SAS_ERR_CUDA; }
+      break;
+    }
+    default:
+      plan_free(pl);
+      sas_set_error("unknown op_kind %d", desc->op_kind);
+      return SAS_ERR_ARG;
+  }
+  cudaError_t e = cudaStreamCreateWithFlags(&pl->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) { plan_free(pl); sas_set_error("stream: %s", cudaGetErrorString(e)); return SAS_ERR_CUDA; }
+#undef TRY
+  *out = pl;
+  return SAS_OK;
+}
+
+extern "C" void sas_plan_destroy(sas_plan* plan) { plan_free(plan); }
+
+extern "C" int sas_plan_info(const sas_plan* pl, int64_t* n, int32_t* r, int32_t* s, int32_t* dtype,
+                             int32_t* op_kind, int32_t* device) {
+  ARG_CHECK(pl, "null plan");
+  if (n) *n = pl->n;
+  if (r) *r = pl->r;
+  if (s) *s = pl->s;
+  if (dtype) *dtype = pl->dtype;
+  if (op_kind) *op_kind = pl->op;
+  if (device) *device = pl->device;
+  return SAS_OK;
+}
+
+extern "C" int32_t sas_last_launch_count(const sas_plan* pl) { return pl ? pl->last_launches : -1; }
+
+// ---------------------------------------------------------------------------
+// K4 launch: pick (NC, RPT) and the CTA size for (s, r).
+template <typename T, int NC, int RPT, class Asm>
+static int launch_lsq_t(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t scratch, cudaStream_t st) {
+  const int W = (a.s + RPT - 1) / RPT;
+  const size_t smem = lsq_smem_bytes<T>(a.s, a.r, W, NC, scratch);
+  auto kern = k_lsq<T, NC, RPT, Asm>;
+  static int configured_dev_mask = 0;
+  (void)configured_dev_mask;
+  SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  SAS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * W, smem));
+  if (occ < 1) {
+    sas_set_error("least-squares kernel does not fit (s=%d r=%d smem=%zu)", a.s, a.r, smem);
+    return SAS_ERR_ARG;
+  }
+  int64_t grid = (int64_t)occ * pl->sms;
+  if (grid > a.P) grid = a.P;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, 32 * W, smem, st>>>(a, as, scratch);
+  SAS_CUDA_CHECK(cudaGetLastError());
+  pl->last_launches++;
+  return SAS_OK;
+}
+
+template <typename T, class Asm>
+static int launch_lsq(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t scratch, cudaStream_t st) {
+  const bool two = (a.r + 1) > 32;
+  if (!two) {
+    if (a.s <= 64) return launch_lsq_t<T, 1, 4>(pl, a, as, scratch, st);
+    if (a.s <= 128) return launch_lsq_t<T, 1, 8>(pl, a, as, scratch, st);
+    if (a.s <= 256) return launch_lsq_t<T, 1, 16>(pl, a, as, scratch, st);
+    return launch_lsq_t<T, 1, 32>(pl, a, as, scratch, st);
+  }
+  if (a.s <= 64) return launch_lsq_t<T, 2, 4>(pl, a, as, scratch, st);
+  if (a.s <= 128) return launch_lsq_t<T, 2, 8>(pl, a, as, scratch, st);
+  return launch_lsq_t<T, 2, 16>(pl, a, as, scratch, st);
+}
+
+// K3 launch
+template <int NT>
+static int launch_gauss_nt(sas_plan* pl, const double* params, int64_t P, double* Mout, cudaStream_t st) {
+  constexpr int PW = 4;
+  const int nw = (pl->s + 7) / 8;
+  if (nw > 12) {
+    sas_set_error("gauss rows: s=%d > 96 not supported", pl->s);
+    return SAS_ERR_ARG;
+  }
+  const size_t smem = gauss_smem_bytes<NT, PW>(nw * 8);
+  auto kern = k_gauss_rows<NT, PW>;
+  SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t grid = (P + PW - 1) / PW;
+  kern<<<(unsigned)grid, 32 * nw, smem, st>>>(pl->D, (const double*)pl->X, pl->S, params, P, pl->s, pl->n,
+                                             pl->r, pl->ridge, Mout);
+  SAS_CUDA_CHECK(cudaGetLastError());
+  pl->last_launches++;
+  return SAS_OK;
+}
+
+static int launch_gauss(sas_plan* pl, const double* params, int64_t P, double* Mout, cudaStream_t st) {
+  const int nt = (pl->r + 7) / 8;
+  switch (nt) {
+    case 1: return launch_gauss_nt<1>(pl, params, P, Mout, st);
+    case 2: return launch_gauss_nt<2>(pl, params, P, Mout, st);
+    case 3: return launch_gauss_nt<3>(pl, params, P, Mout, st);
+    case 4: return launch_gauss_nt<4>(pl, params, P, Mout, st);
+    case 5: return launch_gauss_nt<5>(pl, params, P, Mout, st);
+    case 6: return launch_gauss_nt<6>(pl, params, P, Mout, st);
+    case 7: return launch_gauss_nt<7>(pl, params, P, Mout, st);
+    case 8: return launch_gauss_nt<8>(pl, params, P, Mout, st);
+    default:
+      sas_set_error("gauss rows: r=%d > 64", pl->r);
+      return SAS_ERR_ARG;
+  }
+}
+
+template <typename T>
+static int solve_t(sas_plan* pl, const void* params, int64_t P, const double* coef_table,
+                   const void* rhs_table, void* coef, double* sres, double* outv, int32_t* status,
+                   int32_t* badcol, cudaStream_t st) {
+  LsqArgs<T> a;
+  a.s = pl->s;
+  a.r = pl->r;
+  a.P = P;
+  a.w = pl->w;
+  a.t = rhs_table ? (const T*)rhs_table : (const T*)pl->t;
+  a.t_stride = rhs_table ? pl->s : 0;
+  a.proj = (const T*)pl->proj;
+  a.coef = (T*)coef;
+  a.sres = sres;
+  a.outv = outv;
+  a.status = status;
+  a.badcol = badcol;
+  ParamView pv{(const double*)params, pl->dp, pl->pcomplex};
+  switch (pl->op) {
+    case SAS_OP_AFFINE: {
+      for (int k = 0; k < pl->K; ++k)
+        ARG_CHECK(pl->h_kind[k] != SAS_COEF_TABLE || coef_table, "affine: coefficient table required for SAS_COEF_TABLE terms");
+      AsmAffine<T> as{pl->K, (const T*)pl->blocks, pl->kind, pl->scale, pl->rate, pv, coef_table};
+      return launch_lsq<T>(pl, a, as, AsmAffine<T>::scratch_bytes(0, 0), st);
+    }
+    case SAS_OP_STENCIL: {
+      if constexpr (std::is_same<T, double>::value) {
+        AsmStencil as{pl->E, pl->dp, pl->phi, pl->G, pl->hh, (const double*)params};
+        return launch_lsq<double>(pl, a, as, AsmStencil::scratch_bytes(pl->s, pl->E), st);
+      }
+      sas_set_error("stencil: complex not supported");
+      return SAS_ERR_ARG;
+    }
+    case SAS_OP_GAUSS: {
+      if constexpr (std::is_same<T, double>::value) {
+        // chunk over P so the M scratch stays L2-resident (~64 MB)
+        const int64_t per = (int64_t)pl->s * pl->r * (int64_t)sizeof(double);
+        int64_t chunk = (64ll << 20) / per;
+        chunk = chunk < 4 ? 4 : (chunk / 4) * 4;
+        if (chunk > P) chunk = ((P + 3) / 4) * 4;
+        int rc = ensure(&pl->Mscr, &pl->Mscr_P, chunk * per);
+        if (rc) return rc;
+        for (int64_t p0 = 0; p0 < P; p0 += chunk) {
+          const int64_t pc = (P - p0 < chunk) ? (P - p0) : chunk;
+          rc = launch_gauss(pl, (const double*)params + p0, pc, pl->Mscr, st);
+          if (rc) return rc;
+          LsqArgs<double> b = a;
+          b.P = pc;
+          b.t = a.t + (rhs_table ? p0 * pl->s : 0);
+          b.coef = a.coef + p0 * pl->r;
+          b.sres = sres + p0;
+          b.outv = outv ? outv + 2 * p0 : nullptr;
+          b.status = status + p0;
+          b.badcol = badcol ? badcol + p0 : nullptr;
+          AsmGlobal<double> as{pl->Mscr};
+          rc = launch_lsq<double>(pl, b, as, 0, st);
+          if (rc) return rc;
+        }
+        return SAS_OK;
+      }
+      sas_set_error("gauss: complex not supported");
+      return SAS_ERR_ARG;
+    }
+  }
+  sas_set_error("bad op");
+  return SAS_ERR_ARG;
+}
+
+extern "C" int sas_solve(sas_plan* pl, const void* params, int64_t P, const double* coef_table,
+                         const void* rhs_table, void* coef, double* sres, double* outv, int32_t* status,
+                         int32_t* badcol, void* stream) {
+  ARG_CHECK(pl, "null plan");
+  ARG_CHECK(P >= 0, "P must be >= 0");
+  pl->last_launches = 0;
+  if (P == 0) return SAS_OK;
+  ARG_CHECK(params && coef && sres && status, "sas_solve: params, coef, sampled_res and status are required");
+  DevGuard g(pl->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (pl->dtype == SAS_C128)
+    return solve_t<cplx>(pl, params, P, coef_table, rhs_table, coef, sres, outv, status, badcol, st);
+  return solve_t<double>(pl, params, P, coef_table, rhs_table, coef, sres, outv, status, badcol, st);
+}
+
+extern "C" int sas_solve_host(sas_plan* pl, const void* params, int64_t P, const double* coef_table,
+                              const void* rhs_table, void* coef, double* sres, double* outv,
+                              int32_t* status, int32_t* badcol) {
+  ARG_CHECK(pl, "null plan");
+  ARG_CHECK(P >= 0, "P must be >= 0");
+  if (P == 0) { pl->last_launches = 0; return SAS_OK; }
+  ARG_CHECK(params && coef && sres && status, "sas_solve_host: params, coef, sampled_res and status are required");
+  DevGuard g(pl->device);
+  cudaStream_t st = pl->stream;
+  const int64_t pbytes = P * pl->dp * (pl->pcomplex ? 16 : 8);
+  int rc;
+  if ((rc = ensure(&pl->h_params, &pl->h_params_n, pbytes))) return rc;
+  SAS_CUDA_CHECK(cudaMemcpyAsync(pl->h_params, params, pbytes, cudaMemcpyHostToDevice, st));
+  const double* ctab_d = nullptr;
+  if (coef_table) {
+    const int64_t b = P * pl->K * 16;
+    if ((rc = ensure(&pl->h_ctab, &pl->h_ctab_n, b))) return rc;
+    SAS_CUDA_CHECK(cudaMemcpyAsync(pl->h_ctab, coef_table, b, cudaMemcpyHostToDevice, st));
+    ctab_d = (const double*)pl->h_ctab;
+  }
+  const void* rhs_d = nullptr;
+  if (rhs_table) {
+    const int64_t b = P * pl->s * (int64_t)pl->esz;
+    if ((rc = ensure(&pl->h_rhs, &pl->h_rhs_n, b))) return rc;
+    SAS_CUDA_CHECK(cudaMemcpyAsync(pl->h_rhs, rhs_table, b, cudaMemcpyHostToDevice, st));
+    rhs_d = pl->h_rhs;
+  }
+  const int64_t cb = P * pl->r * (int64_t)pl->esz;
+  if ((rc = ensure(&pl->h_coef, &pl->h_coef_n, cb))) return rc;
+  if ((rc = ensure(&pl->h_sres, &pl->h_sres_n, P * 8))) return rc;
+  if ((rc = ensure(&pl->h_status, &pl->h_status_n, P * 4))) return rc;
+  if (outv && (rc = ensure(&pl->h_outv, &pl->h_outv_n, P * 16))) return rc;
+  if (badcol && (rc = ensure(&pl->h_bad, &pl->h_bad_n, P * 4))) return rc;
+  rc = sas_solve(pl, pl->h_params, P, ctab_d, rhs_d, pl->h_coef, pl->h_sres, outv ? pl->h_outv : nullptr,
+                 pl->h_status, badcol ? pl->h_bad : nullptr, st);
+  if (rc) return rc;
+  SAS_CUDA_CHECK(cudaMemcpyAsync(coef, pl->h_coef, cb, cudaMemcpyDeviceToHost, st));
+  SAS_CUDA_CHECK(cudaMemcpyAsync(sres, pl->h_sres, P * 8, cudaMemcpyDeviceToHost, st));
+  SAS_CUDA_CHECK(cudaMemcpyAsync(status, pl->h_status, P * 4, cudaMemcpyDeviceToHost, st));
+  if (outv) SAS_CUDA_CHECK(cudaMemcpyAsync(outv, pl->h_outv, P * 16, cudaMemcpyDeviceToHost, st));
+  if (badcol) SAS_CUDA_CHECK(cudaMemcpyAsync(badcol, pl->h_bad, P * 4, cudaMemcpyDeviceToHost, st));
+  SAS_CUDA_CHECK(cudaStreamSynchronize(st));
+  return SAS_OK;
+}
+
+extern "C" int sas_lift(sas_plan* pl, const void* coef, int64_t P, void* x, void* stream) {
+  ARG_CHECK(pl, "null plan");
+  if (P == 0) return SAS_OK;
+  ARG_CHECK(coef && x, "sas_lift: coef and x required");
+  DevGuard g(pl->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  dim3 grid((unsigned)((pl->n + 255) / 256), (unsigned)((P + kLiftPT - 1) / kLiftPT));
+  ARG_CHECK(grid.y <= 65535, "sas_lift: P too large for one call (max %d)", 65535 * kLiftPT);
+  if (pl->dtype == SAS_C128)
+    k_lift<cplx><<<grid, 256, 0, st>>>((const cplx*)pl->X, pl->n, pl->r, (const cplx*)coef, P, (cplx*)x);
+  else
+    k_lift<double><<<grid, 256, 0, st>>>((const double*)pl->X, pl->n, pl->r, (const double*)coef, P, (double*)x);
+  SAS_CUDA_CHECK(cudaGetLastError());
+  pl->last_launches = 1;
+  return SAS_OK;
+}
+
+extern "C" int sas_plan_set_operator(sas_plan* pl, const int64_t* const* row_ptr, const int64_t* const* col,
+                                     const void* const* val, const int64_t* nbr_full, const double* phi_full,
+                                     const void* b_full) {
+  ARG_CHECK(pl, "null plan");
+  ARG_CHECK(b_full, "set_operator: b required");
+  DevGuard g(pl->device);
+  int rc;
+  if (pl->full_b) { cudaFree(pl->full_b); pl->full_b = nullptr; }
+  if ((rc = dupload(&pl->full_b, b_full, (size_t)pl->n * pl->esz))) return rc;
+  if (pl->op == SAS_OP_STENCIL) {
+    ARG_CHECK(nbr_full && phi_full, "set_operator: stencil needs nbr and phi");
+    if (pl->full_nbr) cudaFree(pl->full_nbr);
+    if (pl->full_phi) cudaFree(pl->full_phi);
+    pl->full_nbr = nullptr;
+    pl->full_phi = nullptr;
+    if ((rc = dupload(&pl->full_nbr, nbr_full, (size_t)pl->n * pl->E * sizeof(int64_t)))) return rc;
+    if ((rc = dupload(&pl->full_phi, phi_full, (size_t)pl->n * pl->E * pl->dp * sizeof(double)))) return rc;
+  } else if (pl->op == SAS_OP_AFFINE) {
+    ARG_CHECK(row_ptr && col && val, "set_operator: affine needs CSR arrays");
+    for (auto* p : pl->csr_rp) cudaFree(p);
+    for (auto* p : pl->csr_ci) cudaFree(p);
+    for (auto* p : pl->csr_va) cudaFree(p);
+    pl->csr_rp.assign(pl->K, nullptr);
+    pl->csr_ci.assign(pl->K, nullptr);
+    pl->csr_va.assign(pl->K, nullptr);
+    for (int k = 0; k < pl->K; ++k) {
+      const int64_t nnz = row_ptr[k][pl->n];
+      if ((rc = dupload(&pl->csr_rp[k], row_ptr[k], (size_t)(pl->n + 1) * sizeof(int64_t)))) return rc;
+      if ((rc = dupload(&pl->csr_ci[k], col[k], (size_t)nnz * sizeof(int64_t)))) return rc;
+      if ((rc = dupload(&pl->csr_va[k], val[k], (size_t)nnz * pl->esz))) return rc;
+    }
+    if (!pl->csr_rp_d && (rc = dalloc(&pl->csr_rp_d, 16 * sizeof(void*)))) return rc;
+    if (!pl->csr_ci_d && (rc = dalloc(&pl->csr_ci_d, 16 * sizeof(void*)))) return rc;
+    if (!pl->csr_va_d && (rc = dalloc(&pl->csr_va_d, 16 * sizeof(void*)))) return rc;
+    SAS_CUDA_CHECK(cudaMemcpy(pl->csr_rp_d, pl->csr_rp.data(), pl->K * sizeof(void*), cudaMemcpyHostToDevice));
+    SAS_CUDA_CHECK(cudaMemcpy(pl->csr_ci_d, pl->csr_ci.data(), pl->K * sizeof(void*), cudaMemcpyHostToDevice));
+    SAS_CUDA_CHECK(cudaMemcpy(pl->csr_va_d, pl->csr_va.data(), pl->K * sizeof(void*), cudaMemcpyHostToDevice));
+  }
+  return SAS_OK;
+}
+
+template <typename T>
+__global__ void k_affine_coefs(const int32_t* kind, const double* scale, const double* rate, int K, ParamView pv,
+                               const double* ctab, int64_t P, T* f) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= P * K) return;
+  int64_t p = idx / K;
+  int k = (int)(idx - p * K);
+  cplx sc{scale[2 * k], scale[2 * k + 1]};
+  cplx rt{rate[2 * k], rate[2 * k + 1]};
+  f[idx] = AffineCoef<T>::eval(kind[k], sc, rt, pv.get(p, 0), ctab ? ctab + idx * 2 : nullptr);
+}
+
+extern "C" int sas_residual(sas_plan* pl, const void* params, const void* coef, int64_t P, double* relres,
+                            void* stream) {
+  ARG_CHECK(pl, "null plan");
+  if (P == 0) return SAS_OK;
+  ARG_CHECK(params && coef && relres, "sas_residual: params, coef, relres required");
+  ARG_CHECK(pl->full_b, "sas_residual: call sas_plan_set_operator first");
+  ARG_CHECK(P <= 65535, "sas_residual: at most 65535 parameter values per call");
+  DevGuard g(pl->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  int nb = (int)((pl->n + 255) / 256);
+  if (nb > pl->sms * 4) nb = pl->sms * 4;
+  int rc;
+  if ((rc = ensure(&pl->rpart, &pl->rpart_n, P * nb * 2 * (int64_t)sizeof(double)))) return rc;
+  pl->last_launches = 0;
+  dim3 grid(nb, (unsigned)P);
+  if (pl->op == SAS_OP_STENCIL) {
+    ARG_CHECK(pl->full_nbr, "sas_residual: stencil operator not set");
+    k_resid_stencil<<<grid, 256, 0, st>>>((const double*)pl->X, pl->n, pl->r, pl->full_nbr, pl->full_phi, pl->E,
+                                          pl->dp, pl->hh, (const double*)pl->full_b, (const double*)params,
+                                          (const double*)coef, pl->rpart);
+    pl->last_launches++;
+  } else if (pl->op == SAS_OP_AFFINE) {
+    ARG_CHECK(!pl->csr_rp.empty(), "sas_residual: affine operator not set");
+    for (int k = 0; k < pl->K; ++k)
+      ARG_CHECK(pl->h_kind[k] != SAS_COEF_TABLE, "sas_residual: table coefficients not supported");
+    if ((rc = ensure(&pl->fco, &pl->fco_n, P * pl->K * (int64_t)pl->esz))) return rc;
+    ParamView pv{(const double*)params, pl->dp, pl->pcomplex};
+    const int64_t tot = P * pl->K;
+    if (pl->dtype == SAS_C128) {
+      k_affine_coefs<cplx><<<(unsigned)((tot + 127) / 128), 128, 0, st>>>(pl->kind, pl->scale, pl->rate, pl->K, pv,
+                                                                          nullptr, P, (cplx*)pl->fco);
+      k_resid_affine<cplx><<<grid, 256, 0, st>>>((const cplx*)pl->X, pl->n, pl->r, pl->K, pl->csr_rp_d,
+                                                 pl->csr_ci_d, (const cplx* const*)pl->csr_va_d,
+                                                 (const cplx*)pl->fco, (const cplx*)pl->full_b,
+                                                 (const cplx*)coef, pl->rpart);
+    } else {
+      k_affine_coefs<double><<<(unsigned)((tot + 127) / 128), 128, 0, st>>>(pl->kind, pl->scale, pl->rate, pl->K,
+                                                                            pv, nullptr, P, (double*)pl->fco);
+      k_resid_affine<double><<<grid, 256, 0, st>>>((const double*)pl->X, pl->n, pl->r, pl->K, pl->csr_rp_d,
+                                                   pl->csr_ci_d, (const double* const*)pl->csr_va_d,
+                                                   (const double*)pl->fco, (const double*)pl->full_b,
+                                                   (const double*)coef, pl->rpart);
+    }
+    pl->last_launches += 2;
+  } else {
+    // Gaussian kernel: lift x first (P x n scratch), then re-evaluate kernel rows.
+    double* xs = nullptr;
+    if ((rc = dalloc(&xs, (size_t)P * pl->n * sizeof(double)))) return rc;
+    dim3 lg((unsigned)((pl->n + 255) / 256), (unsigned)((P + kLiftPT - 1) / kLiftPT));
+    k_lift<double><<<lg, 256, 0, st>>>((const double*)pl->X, pl->n, pl->r, (const double*)coef, P, xs);
+    k_resid_gauss<<<grid, 256, 0, st>>>((const double*)pl->X, pl->n, pl->r, pl->pts, pl->pdim, pl->ridge,
+                                        (const double*)pl->full_b, (const double*)params, xs, pl->rpart);
+    cudaError_t e = cudaStreamSynchronize(st);
+    cudaFree(xs);
+    if (e != cudaSuccess) { sas_set_error("gauss residual: %s", cudaGetErrorString(e)); return SAS_ERR_CUDA; }
+    pl->last_launches += 2;
+  }
+  k_resid_finish<<<(unsigned)((P + 127) / 128), 128, 0, st>>>(pl->rpart, nb, P, relres);
+  pl->last_launches++;
+  SAS_CUDA_CHECK(cudaGetLastError());
+  return SAS_OK;
+}

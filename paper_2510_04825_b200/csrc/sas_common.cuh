@@ -1,0 +1,218 @@
+// Common device helpers for the SubApSnap online-phase kernels (sm_100a).
+//
+// * cplx: complex128 with the exact operation order numpy uses for complex128
+//   (a+bi)(c+di) = (ac - bd) + (ad + bc)i, evaluated without FMA contraction
+//   where bitwise agreement with the reference's affine combine matters
+//   (online.py:108-112).
+// * Scalar traits so the least-squares kernel is one template for f64 and c128.
+// * sas_exp64: table(64)+degree-5 exp for the kernel-row contraction, ~10 FP64
+//   pipe ops instead of the ~24-DFMA-equivalent libdevice exp (measured on B200,
+//   profiles/r01_fp64_peaks.jsonl).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define SAS_HD __host__ __device__ __forceinline__
+
+struct cplx {
+  double re, im;
+};
+
+SAS_HD cplx mk(double re, double im) { return cplx{re, im}; }
+
+// ---- exact (no-FMA) complex ops, matching numpy complex128 ufuncs ----------
+SAS_HD cplx cmul_exact(cplx a, cplx b) {
+#ifdef __CUDA_ARCH__
+  return cplx{__dsub_rn(__dmul_rn(a.re, b.re), __dmul_rn(a.im, b.im)),
+              __dadd_rn(__dmul_rn(a.re, b.im), __dmul_rn(a.im, b.re))};
+#else
+  volatile double t0 = a.re * b.re, t1 = a.im * b.im, t2 = a.re * b.im, t3 = a.im * b.re;
+  return cplx{t0 - t1, t2 + t3};
+#endif
+}
+SAS_HD cplx cadd_exact(cplx a, cplx b) {
+#ifdef __CUDA_ARCH__
+  return cplx{__dadd_rn(a.re, b.re), __dadd_rn(a.im, b.im)};
+#else
+  return cplx{a.re + b.re, a.im + b.im};
+#endif
+}
+SAS_HD double dmul_exact(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dmul_rn(a, b);
+#else
+  volatile double t = a * b;
+  return t;
+#endif
+}
+SAS_HD double dadd_exact(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dadd_rn(a, b);
+#else
+  volatile double t = a + b;
+  return t;
+#endif
+}
+SAS_HD double dsub_exact(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dsub_rn(a, b);
+#else
+  volatile double t = a - b;
+  return t;
+#endif
+}
+
+// ---- scalar traits ----------------------------------------------------------
+template <typename T>
+struct Sc;
+
+template <>
+struct Sc<double> {
+  static SAS_HD double zero() { return 0.0; }
+  static SAS_HD double from(double re, double) { return re; }
+  static SAS_HD double conj(double a) { return a; }
+  static SAS_HD double abs2(double a) { return a * a; }
+  static SAS_HD double abs(double a) { return fabs(a); }
+  static SAS_HD double re(double a) { return a; }
+  static SAS_HD double im(double) { return 0.0; }
+  // acc + conj(a) * b
+  static SAS_HD double fma_conj(double a, double b, double acc) { return fma(a, b, acc); }
+  // acc - a * b
+  static SAS_HD double fms(double a, double b, double acc) { return fma(-a, b, acc); }
+  static SAS_HD double mul(double a, double b) { return a * b; }
+  static SAS_HD double mulr(double a, double b) { return a * b; }  // scalar * real
+  static SAS_HD double add(double a, double b) { return a + b; }
+  static SAS_HD double sub(double a, double b) { return a - b; }
+  static SAS_HD double div(double a, double b) { return a / b; }
+  static SAS_HD bool finite(double a) { return isfinite(a); }
+  static SAS_HD double mul_exact(double a, double b) { return dmul_exact(a, b); }
+  static SAS_HD double add_exact(double a, double b) { return dadd_exact(a, b); }
+};
+
+template <>
+struct Sc<cplx> {
+  static SAS_HD cplx zero() { return cplx{0.0, 0.0}; }
+  static SAS_HD cplx from(double re, double im) { return cplx{re, im}; }
+  static SAS_HD cplx conj(cplx a) { return cplx{a.re, -a.im}; }
+  static SAS_HD double abs2(cplx a) { return a.re * a.re + a.im * a.im; }
+  static SAS_HD double abs(cplx a) { return hypot(a.re, a.im); }
+  static SAS_HD double re(cplx a) { return a.re; }
+  static SAS_HD double im(cplx a) { return a.im; }
+  static SAS_HD cplx fma_conj(cplx a, cplx b, cplx acc) {
+    // conj(a) * b = (ar br + ai bi) + i (ar bi - ai br)
+    acc.re = fma(a.re, b.re, acc.re);
+    acc.re = fma(a.im, b.im, acc.re);
+    acc.im = fma(a.re, b.im, acc.im);
+    acc.im = fma(-a.im, b.re, acc.im);
+    return acc;
+  }
+  static SAS_HD cplx fms(cplx a, cplx b, cplx acc) {
+    acc.re = fma(-a.re, b.re, acc.re);
+    acc.re = fma(a.im, b.im, acc.re);
+    acc.im = fma(-a.re, b.im, acc.im);
+    acc.im = fma(-a.im, b.re, acc.im);
+    return acc;
+  }
+  static SAS_HD cplx mul(cplx a, cplx b) {
+    return cplx{fma(a.re, b.re, -a.im * b.im), fma(a.re, b.im, a.im * b.re)};
+  }
+  static SAS_HD cplx mulr(cplx a, double b) { return cplx{a.re * b, a.im * b}; }
+  static SAS_HD cplx add(cplx a, cplx b) { return cplx{a.re + b.re, a.im + b.im}; }
+  static SAS_HD cplx sub(cplx a, cplx b) { return cplx{a.re - b.re, a.im - b.im}; }
+  static SAS_HD cplx div(cplx a, cplx b) {
+    // Smith's algorithm (robust against overflow)
+    if (fabs(b.re) >= fabs(b.im)) {
+      double rt = b.im / b.re, den = b.re + b.im * rt;
+      return cplx{(a.re + a.im * rt) / den, (a.im - a.re * rt) / den};
+    } else {
+      double rt = b.re / b.im, den = b.re * rt + b.im;
+      return cplx{(a.re * rt + a.im) / den, (a.im * rt - a.re) / den};
+    }
+  }
+  static SAS_HD bool finite(cplx a) { return isfinite(a.re) && isfinite(a.im); }
+  static SAS_HD cplx mul_exact(cplx a, cplx b) { return cmul_exact(a, b); }
+  static SAS_HD cplx add_exact(cplx a, cplx b) { return cadd_exact(a, b); }
+};
+
+// ---- fast FP64 exp ----------------------------------------------------------
+// e^x = 2^(k/64) * e^r,  k = rint(x*64/ln2),  r = x - k*ln2/64 (two-constant
+// Cody-Waite), |r| <= ln2/128.  e^r - 1 by degree-5 Taylor (truncation
+// r^6/720 <= 3.4e-17).  2^(j/64), j = k mod 64, comes from a 64-entry table held
+// in two registers per lane and fetched with warp shuffles (conflict-free, no
+// shared memory).  2^(k div 64) is applied to the exponent field.  Inputs
+// below -708.39 return 0 (the true value is subnormal, < 2.3e-308); the kernels
+// only evaluate x <= 0.
+// Exact split of ln2/64: hi has its low 20 mantissa bits zero so k*hi is exact
+// for |k| < 2^20; lo = ln2/64 - hi.  Values from mpmath at 50 digits.
+#define SAS_LN2D64_HI 0x1.62e42fef00000p-7
+#define SAS_LN2D64_LO 0x1.473de6af278edp-40
+#define SAS_INVLN2X64 0x1.71547652b82fep+6
+#define SAS_EXP_MAGIC 0x1.8p52
+
+// 2^(j/64), j = 0..63 (correctly rounded; libsas is a single translation unit).
+__constant__ double c_exp2_tab64[64] = {
+    0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
+    0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0,
+    0x1.172b83c7d517bp+0, 0x1.1a35beb6fcb75p+0, 0x1.1d4873168b9aap+0, 0x1.2063b88628cd6p+0,
+    0x1.2387a6e756238p+0, 0x1.26b4565e27cddp+0, 0x1.29e9df51fdee1p+0, 0x1.2d285a6e4030bp+0,
+    0x1.306fe0a31b715p+0, 0x1.33c08b26416ffp+0, 0x1.371a7373aa9cbp+0, 0x1.3a7db34e59ff7p+0,
+    0x1.3dea64c123422p+0, 0x1.4160a21f72e2ap+0, 0x1.44e086061892dp+0, 0x1.486a2b5c13cd0p+0,
+    0x1.4bfdad5362a27p+0, 0x1.4f9b2769d2ca7p+0, 0x1.5342b569d4f82p+0, 0x1.56f4736b527dap+0,
+    0x1.5ab07dd485429p+0, 0x1.5e76f15ad2148p+0, 0x1.6247eb03a5585p+0, 0x1.6623882552225p+0,
+    0x1.6a09e667f3bcdp+0, 0x1.6dfb23c651a2fp+0, 0x1.71f75e8ec5f74p+0, 0x1.75feb564267c9p+0,
+    0x1.7a11473eb0187p+0, 0x1.7e2f336cf4e62p+0, 0x1.82589994cce13p+0, 0x1.868d99b4492edp+0,
+    0x1.8ace5422aa0dbp+0, 0x1.8f1ae99157736p+0, 0x1.93737b0cdc5e5p+0, 0x1.97d829fde4e50p+0,
+    0x1.9c49182a3f090p+0, 0x1.a0c667b5de565p+0, 0x1.a5503b23e255dp+0, 0x1.a9e6b5579fdbfp+0,
+    0x1.ae89f995ad3adp+0, 0x1.b33a2b84f15fbp+0, 0x1.b7f76f2fb5e47p+0, 0x1.bcc1e904bc1d2p+0,
+    0x1.c199bdd85529cp+0, 0x1.c67f12e57d14bp+0, 0x1.cb720dcef9069p+0, 0x1.d072d4a07897cp+0,
+    0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
+    0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0};
+
+
+// Per-lane table registers: lo = 2^(lane/64), hi = 2^((lane+32)/64).
+struct ExpTab {
+  double lo, hi;
+};
+
+__device__ __forceinline__ ExpTab exp_tab_load(int lane) {
+  return ExpTab{c_exp2_tab64[lane], c_exp2_tab64[lane + 32]};
+}
+
+// All 32 lanes of the warp must call this together (warp shuffles).
+__device__ __forceinline__ double sas_exp64(double x, const ExpTab& tab) {
+  double kd = fma(x, SAS_INVLN2X64, SAS_EXP_MAGIC);
+  int ki = __double2loint(kd);
+  double kf = kd - SAS_EXP_MAGIC;
+  double r = fma(-kf, SAS_LN2D64_HI, x);
+  r = fma(-kf, SAS_LN2D64_LO, r);
+  // e^r - 1 = r (1 + r/2 + r^2/6 + r^3/24 + r^4/120)
+  double q = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+  q = fma(q, r, 1.0 / 6.0);
+  q = fma(q, r, 0.5);
+  q = fma(q, r, 1.0);
+  q = q * r;
+  int j = ki & 63;
+  double tlo = __shfl_sync(0xffffffffu, tab.lo, j & 31);
+  double thi = __shfl_sync(0xffffffffu, tab.hi, j & 31);
+  double t = (j & 32) ? thi : tlo;
+  double res = fma(t, q, t);  // in [0.99, 2.01)
+  int e = ki >> 6;            // floor(k / 64)
+  int hi = __double2hiint(res) + (e << 20);
+  res = __hiloint2double(hi, __double2loint(res));
+  return (x < -708.39) ? 0.0 : res;
+}
+
+// Host reference of the same algorithm (for the CPU accuracy test).
+double sas_exp64_host(double x);
+
+#define SAS_CUDA_CHECK(expr)                                                   \
+  do {                                                                         \
+    cudaError_t _e = (expr);                                                   \
+    if (_e != cudaSuccess) {                                                   \
+      sas_set_error("CUDA error %s at %s:%d: %s", cudaGetErrorName(_e),        \
+                    __FILE__, __LINE__, cudaGetErrorString(_e));               \
+      return SAS_ERR_CUDA;                                                     \
+    }                                                                          \
+  } while (0)
+
+void sas_set_error(const char* fmt, ...);

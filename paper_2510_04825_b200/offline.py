@@ -1,0 +1,402 @@
+"""Offline-phase inputs of the online path: snapshot basis X and row selector S.
+
+The offline phase is not on the hot path (BASELINE.json north_star: "the
+offline snapshot solves and subsample selection stay in the reference and are
+timed separately").  On the GPU box the reference is not available, and its
+SuperLU snapshot solves are impractical at the BASELINE sizes,
+so this module restates the reference's offline recipe with the same
+semantics and data types to produce X and S there:
+
+  SnapshotBasis, build_snapshot(mode qr | pod(tol) | none)   snapshot.py:14-34, 79-134
+  RowSelector, select_rows(strategy leverage | random)        subsample.py:22-67, 95-156
+  choose_anchor                                               subsample.py:198-209
+  save/load_snapshot, save/load_selector (reference formats)  snapshot.py:137-158, subsample.py:212-235
+
+Snapshot solves use a harness solver per operator kind (documented in
+DESIGN.md): sparse direct (scipy) for affine/stencil systems small enough for
+it, dense Cholesky for the Gaussian kernel (torch on the GPU when available),
+preconditioned CG on the GPU for large SPD stencils.  Each solve carries the
+reference's residual guard (systems.py:187-222).
+"""
+from __future__ import annotations
+
+import json
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+from .errors import ConfigError, NumericalError, RankDeficiencyError
+from .systems import GaussianKernelOperator, StencilOperator
+
+FULL_SOLVE_RTOL = 1e-10
+
+
+@dataclass(frozen=True)
+class SnapshotBasis:
+    points: tuple
+    raw: np.ndarray
+    basis: np.ndarray
+    singular_values: np.ndarray
+
+    @property
+    def n(self) -> int:
+        return self.basis.shape[0]
+
+    @property
+    def rank(self) -> int:
+        return self.basis.shape[1]
+
+
+@dataclass(frozen=True)
+class RowSelector:
+    indices: np.ndarray
+    n: int
+    weights: Optional[np.ndarray] = None
+    strategy: str = ""
+    anchors: tuple = ()
+
+    def __post_init__(self):
+        object.__setattr__(self, "indices", np.asarray(self.indices, dtype=np.int64))
+        if self.weights is not None:
+            object.__setattr__(self, "weights", np.asarray(self.weights, dtype=float))
+            if self.weights.shape != self.indices.shape:
+                raise ValueError("weights/indices length mismatch")
+            if np.any(self.weights <= 0):
+                raise ValueError("weights must be positive")
+        if self.indices.size and (self.indices.min() < 0 or self.indices.max() >= self.n):
+            raise ValueError("selector index out of range")
+
+    @property
+    def size(self) -> int:
+        return int(self.indices.size)
+
+    def apply(self, m) -> np.ndarray:
+        m = np.asarray(m)
+        out = m[self.indices]
+        if self.weights is not None:
+            out = out * (self.weights[:, None] if out.ndim == 2 else self.weights)
+        return out
+
+
+# --------------------------------------------------------------------------
+# snapshot solves
+# --------------------------------------------------------------------------
+def _guard(a_apply, a_norm, x, b, p):
+    res = np.linalg.norm(a_apply(x) - b)
+    floor = max(a_norm * np.linalg.norm(x) + np.linalg.norm(b), 1e-300)
+    if not np.all(np.isfinite(x)) or res > FULL_SOLVE_RTOL * floor:
+        raise NumericalError(f"full_solve residual {res:.3e} exceeds {FULL_SOLVE_RTOL:.0e} * "
+                             f"(||A|| ||x|| + ||b||) at p={p}")
+
+
+def _sparse_solve(a: sp.csr_matrix, b: np.ndarray, p):
+    """spsolve with up to two refinement steps and the residual guard (systems.py:187-222)."""
+    lu = spla.splu(a.tocsc())
+    x = lu.solve(b.astype(np.result_type(a.dtype, b.dtype)))
+    a_norm = spla.norm(a)
+    floor = lambda x: max(a_norm * np.linalg.norm(x) + np.linalg.norm(b), 1e-300)
+    res = np.linalg.norm(a @ x - b)
+    for _ in range(2):
+        if np.all(np.isfinite(x)) and res <= FULL_SOLVE_RTOL * floor(x):
+            break
+        x = x + lu.solve(b - a @ x)
+        res = np.linalg.norm(a @ x - b)
+    _guard(lambda v: a @ v, a_norm, x, b, p)
+    return x
+
+
+def _gauss_solve_all(op: GaussianKernelOperator, b: np.ndarray, points, device=None):
+    """Dense Cholesky solves of (K_p + ridge I) x = b for every snapshot p."""
+    xs = op.points
+    n = xs.shape[0]
+    cols = []
+    if device is not None:
+        import torch
+        X = torch.from_numpy(xs).to(device)
+        # D_ij = sum_k (x_ik - x_jk)^2, sequential in k (same order as the row oracle)
+        D = torch.zeros((n, n), dtype=torch.float64, device=device)
+        for k in range(xs.shape[1]):
+            df = X[:, k][:, None] - X[:, k][None, :]
+            D += df * df
+        bt = torch.from_numpy(b).to(device)
+        for p in points:
+            inv = 1.0 / (2.0 * p * p)
+            K = torch.exp(-(D * inv))
+            K.diagonal().add_(op.ridge)
+            L = torch.linalg.cholesky(K)
+            x = torch.cholesky_solve(bt[:, None], L)[:, 0]
+            res = torch.linalg.norm(K @ x - bt).item()
+            fl = torch.linalg.norm(K).item() * torch.linalg.norm(x).item() + torch.linalg.norm(bt).item()
+            if not math.isfinite(res) or res > FULL_SOLVE_RTOL * fl:
+                raise NumericalError(f"snapshot solve failed at p={p}: residual {res:.3e}")
+            cols.append(x.cpu().numpy())
+            del K, L
+        return cols
+    import scipy.linalg as sla
+    D = np.zeros((n, n))
+    for k in range(xs.shape[1]):
+        df = xs[:, k][:, None] - xs[:, k][None, :]
+        D += df * df
+    for p in points:
+        inv = 1.0 / (2.0 * p * p)
+        K = np.exp(-(D * inv))
+        K[np.arange(n), np.arange(n)] += op.ridge
+        x = sla.cho_solve(sla.cho_factor(K), b)
+        _guard(lambda v: K @ v, np.linalg.norm(K), x, b, p)
+        cols.append(x)
+    return cols
+
+
+def _stencil_cg(system, p, device, tol=1e-12, maxiter=200_000):
+    """Jacobi-preconditioned CG on the GPU for the SPD stencil operator."""
+    import torch
+    op: StencilOperator = system.operator
+    nbr, phi = op.edges(np.arange(op.n))
+    pv = np.asarray(p, dtype=float).ravel()
+    arg = phi[..., 0] * pv[0]
+    for k in range(1, pv.size):
+        arg = arg + phi[..., k] * pv[k]
+    c = np.exp(arg) / (op.h * op.h)
+    diag = c.sum(axis=1)
+    ct = torch.from_numpy(np.where(nbr >= 0, c, 0.0)).to(device)
+    nt = torch.from_numpy(np.where(nbr >= 0, nbr, 0)).to(device)
+    dg = torch.from_numpy(diag).to(device)
+    b = torch.from_numpy(np.asarray(system.b, dtype=float)).to(device)
+
+    def A(v):
+        return dg * v - (ct * v[nt]).sum(dim=1)
+
+    x = torch.zeros_like(b)
+    r = b.clone()
+    z = r / dg
+    pdir = z.clone()
+    rz = torch.dot(r, z)
+    bn = torch.linalg.norm(b)
+    for it in range(maxiter):
+        Ap = A(pdir)
+        alpha = rz / torch.dot(pdir, Ap)
+        x += alpha * pdir
+        r -= alpha * Ap
+        if it % 50 == 0 and torch.linalg.norm(r) <= tol * bn:
+            break
+        z = r / dg
+        rz_new = torch.dot(r, z)
+        pdir = z + (rz_new / rz) * pdir
+        rz = rz_new
+    r = b - A(x)  # true residual
+    a_norm = float(torch.sqrt((dg * dg).sum() + (ct * ct).sum()))
+    res = float(torch.linalg.norm(r))
+    floor = a_norm * float(torch.linalg.norm(x)) + float(bn)
+    if res > FULL_SOLVE_RTOL * floor:
+        raise NumericalError(f"CG snapshot solve failed at p={p}: residual {res:.3e}")
+    return x.cpu().numpy()
+
+
+def snapshot_solves(system, points, device=None, prefer_cg: bool = False):
+    """Columns x(p_i) = A(p_i)^{-1} b(p_i) with the harness solver for the system."""
+    op = getattr(system, "operator", None)
+    if isinstance(op, GaussianKernelOperator):
+        return _gauss_solve_all(op, np.asarray(system.b, dtype=float), points, device)
+    cols = []
+    for p in points:
+        if isinstance(op, StencilOperator) and (prefer_cg or op.n > 200_000) and device is not None:
+            cols.append(_stencil_cg(system, p, device))
+        else:
+            cols.append(_sparse_solve(system.matrix(p), system.full_rhs(p), p))
+    return cols
+
+
+def _parse_mode(mode):
+    if isinstance(mode, tuple):
+        name, tol = mode
+        return name, float(tol)
+    if isinstance(mode, str) and mode.startswith("pod(") and mode.endswith(")"):
+        return "pod", float(mode[4:-1])
+    if mode == "pod":
+        return "pod", 1e-10
+    return mode, 0.0
+
+
+def orthonormalize(raw: np.ndarray, mode="qr"):
+    """snapshot.py:107-123: thin SVD for sigma, then qr / pod(tol) / none."""
+    _, sigma, _ = np.linalg.svd(raw, full_matrices=False)
+    name, tol = _parse_mode(mode)
+    if name == "qr":
+        q, rmat = np.linalg.qr(raw)
+        diag = np.abs(np.diag(rmat))
+        if diag.size and diag.min() < 1e-12 * max(diag.max(), np.finfo(float).tiny):
+            raise RankDeficiencyError(f"numerically rank-deficient: min |R_ii| = {diag.min():.3e}, "
+                                      f"max |R_ii| = {diag.max():.3e}")
+        basis = q
+    elif name == "pod":
+        w, s, _ = np.linalg.svd(raw, full_matrices=False)
+        keep = s > tol * s[0] if s[0] > 0 else np.ones_like(s, dtype=bool)
+        basis = w[:, :max(int(np.count_nonzero(keep)), 1)]
+    elif name == "none":
+        basis = raw
+    else:
+        raise ConfigError(f"unknown snapshot mode {mode!r}")
+    return basis, sigma
+
+
+def build_snapshot(system, points, mode="qr", device=None, prefer_cg: bool = False) -> SnapshotBasis:
+    points = list(points)
+    if not points:
+        raise ConfigError("no snapshot points given")
+    cols = snapshot_solves(system, points, device=device, prefer_cg=prefer_cg)
+    raw = np.column_stack(cols)
+    basis, sigma = orthonormalize(raw, mode)
+    return SnapshotBasis(points=tuple(points), raw=raw, basis=basis, singular_values=sigma)
+
+
+# --------------------------------------------------------------------------
+# row selection (subsample.py:95-156, 198-209)
+# --------------------------------------------------------------------------
+def choose_anchor(points):
+    pts = list(points)
+
+    def key(p):
+        vec = np.atleast_1d(np.asarray(p, dtype=complex))
+        if vec.size > 1 or vec.imag.any():
+            return float(np.linalg.norm(vec))
+        return float(vec.real[0])
+
+    order = sorted(range(len(pts)), key=lambda k: key(pts[k]))
+    return pts[order[(len(pts) - 1) // 2]]
+
+
+def _range_basis(target, rtol=1e-12):
+    m = np.asarray(target)
+    norms = np.linalg.norm(m, axis=0)
+    norms = np.where(norms == 0, 1.0, norms)
+    w, s, _ = np.linalg.svd(m / norms, full_matrices=False)
+    if s[0] == 0:
+        raise RankDeficiencyError("zero matrix has no range basis")
+    keep = max(int(np.count_nonzero(s > rtol * s[0])), 1)
+    return w[:, :keep]
+
+
+def leverage_scores(q) -> np.ndarray:
+    q = np.asarray(q)
+    r = q.shape[1]
+    gram = q.conj().T @ q
+    if np.linalg.norm(gram - np.eye(r)) > 1e-8:
+        raise ValueError("leverage_scores needs orthonormal columns")
+    return np.einsum("ij,ij->i", q.conj(), q).real
+
+
+def select_rows(b, rhs=None, strategy="leverage", oversample=4.0, augment_rhs=True, seed=0,
+                rng=None, anchors=()) -> RowSelector:
+    b = np.asarray(b)
+    n, _ = b.shape
+    if rng is None:
+        rng = np.random.default_rng(seed)
+    target = b
+    if augment_rhs and rhs is not None:
+        target = np.column_stack([b, np.asarray(rhs)])
+    width = target.shape[1]
+    s = int(math.ceil(oversample * width))
+    if strategy == "random":
+        s = min(s, n)
+        idx = np.sort(rng.choice(n, size=s, replace=False))
+        return RowSelector(indices=idx, n=n, strategy=strategy, anchors=tuple(anchors))
+    if strategy == "leverage":
+        q = _range_basis(target)
+        scores = leverage_scores(q)
+        total = scores.sum()
+        if total <= 0:
+            raise RankDeficiencyError("all-zero leverage scores")
+        pi = scores / total
+        idx = rng.choice(n, size=s, replace=True, p=pi)
+        weights = 1.0 / np.sqrt(s * pi[idx])
+        return RowSelector(indices=idx, n=n, weights=weights, strategy=strategy, anchors=tuple(anchors))
+    raise ConfigError(f"strategy {strategy!r} is not restated here (use the reference's select_rows)")
+
+
+def anchor_product(system, anchor, basis, device=None) -> np.ndarray:
+    """B = A(anchor) Q_X (cli.py:247)."""
+    op = getattr(system, "operator", None)
+    X = np.asarray(basis)
+    if isinstance(op, GaussianKernelOperator):
+        xs = op.points
+        n = xs.shape[0]
+        inv = 1.0 / (2.0 * anchor * anchor)
+        if device is not None:
+            import torch
+            P = torch.from_numpy(xs).to(device)
+            D = torch.zeros((n, n), dtype=torch.float64, device=device)
+            for k in range(xs.shape[1]):
+                df = P[:, k][:, None] - P[:, k][None, :]
+                D += df * df
+            K = torch.exp(-(D * inv))
+            K.diagonal().add_(op.ridge)
+            return (K @ torch.from_numpy(X).to(device)).cpu().numpy()
+        D = np.zeros((n, n))
+        for k in range(xs.shape[1]):
+            df = xs[:, k][:, None] - xs[:, k][None, :]
+            D += df * df
+        K = np.exp(-(D * inv))
+        K[np.arange(n), np.arange(n)] += op.ridge
+        return K @ X
+    return np.asarray(system.matrix(anchor) @ X)
+
+
+def offline(problem, device=None, prefer_cg=False, basis: Optional[SnapshotBasis] = None):
+    """Full offline recipe of a problems.Problem: snapshot basis, anchor,
+    leverage selector with `samples` rows (cli.py:239-265)."""
+    system = problem.system
+    if basis is None:
+        basis = build_snapshot(system, problem.snapshot_points, problem.snapshot_mode, device=device,
+                               prefer_cg=prefer_cg)
+    anchor = choose_anchor(basis.points)
+    b_anchor = anchor_product(system, anchor, basis.basis, device=device)
+    rhs_anchor = system.full_rhs(anchor)
+    width = basis.rank + 1
+    sel = select_rows(b_anchor, rhs_anchor, strategy="leverage", oversample=problem.samples / width,
+                      seed=problem.selector_seed, anchors=(anchor,))
+    if sel.size != problem.samples:
+        raise ConfigError(f"selector size {sel.size} != requested samples {problem.samples}")
+    return basis, sel
+
+
+# --------------------------------------------------------------------------
+# artifacts in the reference's formats
+# --------------------------------------------------------------------------
+def save_snapshot(path, basis: SnapshotBasis) -> None:
+    pts = np.array([np.atleast_1d(np.asarray(p, dtype=complex)) for p in basis.points])
+    np.savez_compressed(path, points=pts, raw=basis.raw, basis=basis.basis,
+                        singular_values=basis.singular_values)
+
+
+def load_snapshot(path) -> SnapshotBasis:
+    data = np.load(path)
+    points = []
+    for row in data["points"]:
+        row = np.atleast_1d(row)
+        if row.size == 1:
+            val = complex(row[0])
+            points.append(val.real if val.imag == 0 else val)
+        else:
+            points.append(tuple(complex(v).real if complex(v).imag == 0 else complex(v) for v in row))
+    return SnapshotBasis(points=tuple(points), raw=data["raw"], basis=data["basis"],
+                         singular_values=data["singular_values"])
+
+
+def save_selector(path, selector: RowSelector) -> None:
+    payload = {"n": selector.n, "indices": [int(i) for i in selector.indices],
+               "weights": None if selector.weights is None else [float(w) for w in selector.weights],
+               "strategy": selector.strategy, "anchors": [repr(a) for a in selector.anchors]}
+    with open(path, "w") as fh:
+        json.dump(payload, fh, indent=1)
+
+
+def load_selector(path) -> RowSelector:
+    with open(path) as fh:
+        payload = json.load(fh)
+    return RowSelector(indices=np.array(payload["indices"], dtype=np.int64), n=int(payload["n"]),
+                       weights=None if payload["weights"] is None else np.array(payload["weights"], dtype=float),
+                       strategy=payload["strategy"], anchors=tuple(payload["anchors"]))

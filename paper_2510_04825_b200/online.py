@@ -1,0 +1,522 @@
+"""Online phase on the GPU — drop-in for subapsnap.online.
+
+Same public names, argument order, return types and error behaviour as
+/root/reference/pkg/src/subapsnap/online.py:
+
+  precompute_online(system, basis, selector) -> OnlinePlan      (online.py:68-102)
+  solve_online(plan, p, want_interval=False) -> OnlineSolution  (online.py:105-134)
+  solve_batch(plan, parameters, want_interval=False, workers=1) (online.py:208-225)
+  estimate_residual(plan, solution)                            (online.py:137-153)
+  OnlineSolution.lift()                                        (online.py:50-54)
+  save_plan / load_plan                                        (online.py:168-195)
+
+plus the columnar batch API the GPU needs (per-p Python objects would cost
+more than the solve itself):
+
+  solve_params(plan, parameters) -> BatchResult       (host arrays in/out)
+  solve_device(plan, params_tensor, ...) -> tensors   (device-resident, torch)
+  lift_batch(plan, coefficients) -> x (P x n)
+  relative_residual(plan, parameters, coefficients)   (cli.py:344-351 checker)
+
+Every numerical step of the per-parameter solve runs in libsas.so; this
+module only marshals arguments.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _capi
+from .errors import BackendError, RankDeficiencyError
+from .systems import GaussianKernelOperator, StencilOperator
+
+PLAN_CHECK_RTOL = 1e-13
+
+
+# --------------------------------------------------------------------------
+# GPU plan (owner of the libsas handle)
+# --------------------------------------------------------------------------
+_KIND_CODES = {"const": _capi.SAS_COEF_CONST, "linear": _capi.SAS_COEF_LINEAR,
+               "exp": _capi.SAS_COEF_EXP}
+
+
+def _is_complex_value(v) -> bool:
+    return isinstance(v, complex) or np.iscomplexobj(v)
+
+
+class GpuPlan:
+    """libsas plan for one (system, basis, selector) on one CUDA device."""
+
+    def __init__(self, system, basis, selector, blocks, proj, device: int = 0,
+                 force_complex: bool = False):
+        self.lib = _capi.load()
+        self.system = system
+        self.device = int(device)
+        X = np.asarray(basis.basis)
+        self.n, self.r = X.shape
+        idx = np.ascontiguousarray(selector.indices, dtype=np.int64)
+        self.s = idx.size
+        self.dp = int(system.domain.dim) if hasattr(system, "domain") else 1
+        self.pcomplex = bool(getattr(system.domain, "axes", None) and any(a.imag for a in system.domain.axes))
+        terms = system.affine_terms
+        complex_data = (np.iscomplexobj(X) or force_complex or self.pcomplex
+                        or (blocks is not None and any(np.iscomplexobj(b) for b in blocks))
+                        or (proj is not None and np.iscomplexobj(proj)))
+        if terms is not None:
+            for t in terms:
+                for v in (getattr(t, "scale", 0.0), getattr(t, "rate", 0.0)):
+                    if complex(v).imag != 0.0:
+                        complex_data = True
+        self.rhs_constant = getattr(system, "rhs_constant", None)
+        if self.rhs_constant is None:  # duck-typed reference system: rhs_fn is opaque
+            self.rhs_constant = False
+        if self.rhs_constant and np.iscomplexobj(system.b):
+            complex_data = True
+        self.complex = bool(complex_data)
+        self.np_dtype = np.complex128 if self.complex else np.float64
+        # the reference coerces const/linear coefficients to complex (systems.py:92, 98):
+        # keep its result dtype for duck-typed systems whose scales are Python complex
+        self.result_dtype = self.np_dtype
+        if terms is not None and any(isinstance(getattr(t, "scale", None), complex) for t in terms):
+            self.result_dtype = np.complex128
+
+        desc = _capi.SasDesc()
+        desc.dtype = _capi.SAS_C128 if self.complex else _capi.SAS_F64
+        desc.param_dim = self.dp
+        desc.param_complex = 1 if self.pcomplex else 0
+        keep = []  # keep host arrays alive during the call
+        self.table_terms = []
+        op = getattr(system, "operator", None)
+        if terms is not None:
+            K = len(terms)
+            kinds = np.zeros(K, dtype=np.int32)
+            scales = np.zeros((K, 2))
+            rates = np.zeros((K, 2))
+            for k, t in enumerate(terms):
+                kind = getattr(t, "kind", "other")
+                if kind in _KIND_CODES:
+                    kinds[k] = _KIND_CODES[kind]
+                    sc = complex(getattr(t, "scale", 1.0))
+                    rt = complex(getattr(t, "rate", 0.0))
+                    scales[k] = (sc.real, sc.imag)
+                    rates[k] = (rt.real, rt.imag)
+                else:
+                    kinds[k] = _capi.SAS_COEF_TABLE
+                    self.table_terms.append(k)
+            blk = np.ascontiguousarray(np.stack([np.asarray(b) for b in blocks]).astype(self.np_dtype))
+            keep += [kinds, scales, rates, blk]
+            desc.op_kind = _capi.SAS_OP_AFFINE
+            desc.n_terms = K
+            desc.term_kind = kinds.ctypes.data_as(C.POINTER(C.c_int32))
+            desc.term_scale = scales.ctypes.data_as(C.POINTER(C.c_double))
+            desc.term_rate = rates.ctypes.data_as(C.POINTER(C.c_double))
+            desc.blocks = C.c_void_p(blk.ctypes.data)
+            self.K = K
+        elif isinstance(op, StencilOperator):
+            nbr, phi = op.edges(idx)
+            keep += [nbr, phi]
+            desc.op_kind = _capi.SAS_OP_STENCIL
+            desc.n_edges = op.n_edges
+            desc.edge_nbr = nbr.ctypes.data_as(C.POINTER(C.c_int64))
+            desc.edge_phi = phi.ctypes.data_as(C.POINTER(C.c_double))
+            desc.edge_div = op.h * op.h
+            self.K = 0
+        elif isinstance(op, GaussianKernelOperator):
+            pts = np.ascontiguousarray(op.points, dtype=np.float64)
+            keep.append(pts)
+            desc.op_kind = _capi.SAS_OP_GAUSS
+            desc.points = pts.ctypes.data_as(C.POINTER(C.c_double))
+            desc.point_dim = pts.shape[1]
+            desc.ridge = float(op.ridge)
+            self.K = 0
+        else:
+            raise ValueError("system has neither affine terms nor a GPU row operator")
+
+        Xc = np.ascontiguousarray(X.astype(self.np_dtype, copy=False))
+        w = None if selector.weights is None else np.ascontiguousarray(selector.weights, dtype=np.float64)
+        if self.rhs_constant:
+            t = np.ascontiguousarray(np.asarray(system.b)[idx].astype(self.np_dtype))
+        else:
+            t = np.zeros(self.s, dtype=self.np_dtype)
+        pj = None if proj is None else np.ascontiguousarray(np.asarray(proj).astype(self.np_dtype))
+        keep += [Xc, w, t, pj, idx]
+        handle = C.c_void_p()
+        rc = self.lib.sas_plan_create(C.byref(desc), _capi.ptr(Xc), self.n, self.r,
+                                      idx.ctypes.data_as(C.POINTER(C.c_int64)),
+                                      None if w is None else w.ctypes.data_as(C.POINTER(C.c_double)),
+                                      self.s, _capi.ptr(t), _capi.ptr(pj), self.device, 0, C.byref(handle))
+        _capi.check(rc, "sas_plan_create")
+        self.handle = handle
+        self.has_proj = proj is not None
+        self.indices = idx
+        self._operator_set = False
+
+    # -- argument marshalling ------------------------------------------------
+    def params_array(self, parameters) -> np.ndarray:
+        vals = [np.atleast_1d(np.asarray(p, dtype=complex)).ravel() for p in parameters]
+        if any(v.size != self.dp for v in vals):
+            raise ValueError(f"parameters must have {self.dp} component(s)")
+        arr = np.array(vals, dtype=complex).reshape(len(vals), self.dp)
+        if self.pcomplex:
+            return np.ascontiguousarray(np.stack([arr.real, arr.imag], axis=-1))
+        if len(vals) and np.any(arr.imag != 0):
+            raise ValueError("complex parameter for a real-parameter plan")
+        return np.ascontiguousarray(arr.real)
+
+    def coef_table(self, parameters) -> Optional[np.ndarray]:
+        if not self.table_terms:
+            return None
+        tab = np.zeros((len(parameters), self.K, 2))
+        for i, p in enumerate(parameters):
+            for k in self.table_terms:
+                v = complex(self.system.affine_terms[k].coeff(p))
+                tab[i, k] = (v.real, v.imag)
+        return tab
+
+    def rhs_table(self, parameters) -> Optional[np.ndarray]:
+        if self.rhs_constant:
+            return None
+        return np.ascontiguousarray(np.stack([np.asarray(self.system.rhs(p, self.indices)) for p in parameters])
+                                    .astype(self.np_dtype))
+
+    # -- calls -----------------------------------------------------------------
+    def solve_host(self, parameters):
+        P = len(parameters)
+        pa = self.params_array(parameters)
+        ct = self.coef_table(parameters)
+        rt = self.rhs_table(parameters)
+        coef = np.empty((P, self.r), dtype=self.np_dtype)
+        sres = np.empty(P)
+        outv = np.empty((P, 2))
+        status = np.empty(P, dtype=np.int32)
+        bad = np.empty(P, dtype=np.int32)
+        rc = self.lib.sas_solve_host(self.handle, _capi.ptr(pa), P, _capi.ptr(ct), _capi.ptr(rt),
+                                     _capi.ptr(coef), _capi.ptr(sres), _capi.ptr(outv), _capi.ptr(status),
+                                     _capi.ptr(bad))
+        _capi.check(rc, "sas_solve_host")
+        return coef, sres, outv[:, 0] + 1j * outv[:, 1], status, bad
+
+    def launches(self) -> int:
+        return int(self.lib.sas_last_launch_count(self.handle))
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            self.lib.sas_plan_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# --------------------------------------------------------------------------
+# reference data types (online.py:26-54, 198-205)
+# --------------------------------------------------------------------------
+@dataclass(frozen=True)
+class OnlinePlan:
+    system: object
+    basis: object
+    selector: object
+    blocks: Optional[tuple]          # per affine term, s x r' (unweighted)
+    sampled_basis: np.ndarray        # S Q_X, s x r'
+    output_projection: Optional[np.ndarray]  # c^H Q_X
+    gpu: Optional[GpuPlan] = field(default=None, repr=False, compare=False)
+
+    @property
+    def affine(self) -> bool:
+        return self.blocks is not None
+
+
+@dataclass
+class OnlineSolution:
+    parameter: object
+    coefficients: np.ndarray
+    sampled_residual: float
+    residual_interval: Optional[tuple] = None
+    output_value: Optional[complex] = None
+    _basis: object = field(default=None, repr=False)
+    _lifted: Optional[np.ndarray] = field(default=None, repr=False)
+    _plan: object = field(default=None, repr=False)
+
+    def lift(self) -> np.ndarray:
+        """x = Q_X c, computed on the GPU (libsas sas_lift), cached."""
+        if self._lifted is None:
+            if self._plan is not None and self._plan.gpu is not None:
+                self._lifted = lift_batch(self._plan, self.coefficients[None, :])[0]
+            else:
+                self._lifted = self._basis.basis @ self.coefficients
+        return self._lifted
+
+
+@dataclass(frozen=True)
+class BatchRow:
+    parameter: object
+    sampled_residual: float
+    residual_interval: Optional[tuple]
+    output_value: Optional[complex]
+    wall_time: float
+    solution: OnlineSolution
+
+
+@dataclass
+class BatchResult:
+    """Columnar results of solve_params (input order)."""
+
+    parameters: list
+    coefficients: np.ndarray      # P x r'
+    sampled_residual: np.ndarray  # P
+    output_value: Optional[np.ndarray]  # P complex, or None
+    status: np.ndarray            # P int32 (0 ok, 1 rank-deficient, 2 non-finite)
+    bad_column: np.ndarray        # P int32
+    seconds: float
+
+
+# --------------------------------------------------------------------------
+def precompute_online(system, basis, selector, device: int = 0) -> OnlinePlan:
+    """Precompute the selector-row blocks of each affine term (host, as the
+    reference does, online.py:77-85) and build the device plan."""
+    if basis.n != system.n or selector.n != system.n:
+        raise ValueError("system/basis/selector dimension mismatch")
+    idx = np.asarray(selector.indices, dtype=np.int64)
+    uniq, inverse = np.unique(idx, return_inverse=True)
+    sampled_basis = np.asarray(basis.basis)[idx]
+    blocks = None
+    if system.affine_terms is not None:
+        blocks = tuple(np.asarray(term.matrix[uniq] @ basis.basis)[inverse] for term in system.affine_terms)
+    proj = None
+    if system.output_functional is not None:
+        proj = system.output_functional.conj() @ basis.basis
+    gpu = GpuPlan(system, basis, selector, blocks, proj, device=device)
+    return OnlinePlan(system=system, basis=basis, selector=selector, blocks=blocks,
+                      sampled_basis=sampled_basis, output_projection=proj, gpu=gpu)
+
+
+def _gpu(plan: OnlinePlan) -> GpuPlan:
+    if plan.gpu is None:
+        raise BackendError("plan has no device plan (load_plan/precompute_online builds one)")
+    return plan.gpu
+
+
+def solve_params(plan: OnlinePlan, parameters) -> BatchResult:
+    """Solve many parameters in one GPU call; results in input order."""
+    parameters = list(parameters)
+    g = _gpu(plan)
+    t0 = time.perf_counter()
+    coef, sres, outv, status, bad = g.solve_host(parameters)
+    dt = time.perf_counter() - t0
+    coef = coef.astype(g.result_dtype, copy=False)
+    return BatchResult(parameters=parameters, coefficients=coef, sampled_residual=sres,
+                       output_value=outv if g.has_proj else None, status=status, bad_column=bad,
+                       seconds=dt)
+
+
+def _raise_for_status(res: BatchResult):
+    bad = np.nonzero(res.status)[0]
+    if bad.size == 0:
+        return
+    k = int(bad[0])
+    p = res.parameters[k]
+    if res.status[k] == _capi.SAS_ST_RANK_DEFICIENT:
+        raise RankDeficiencyError(
+            f"subsampled system rank-deficient at p={p}: "
+            f"rank-deficient least-squares matrix at column {int(res.bad_column[k])}")
+    raise ValueError("matrix has non-finite entries")
+
+
+def _interval(plan: OnlinePlan, est):
+    sel = plan.selector
+    r = plan.basis.rank
+    eps = min(max(r * math.log(r) / sel.size if r > 1 else 0.0, 0.0), 0.99)
+    return est / (1.0 + eps), est / (1.0 - eps)
+
+
+def _solution(plan, res: BatchResult, k: int, want_interval: bool) -> OnlineSolution:
+    out = None if res.output_value is None else complex(res.output_value[k])
+    sol = OnlineSolution(parameter=res.parameters[k], coefficients=res.coefficients[k].copy(),
+                         sampled_residual=float(res.sampled_residual[k]), output_value=out,
+                         _basis=plan.basis, _plan=plan)
+    if want_interval and plan.selector.weights is not None:
+        _, lower, upper, _ = estimate_residual(plan, sol)
+        sol.residual_interval = (lower, upper)
+    return sol
+
+
+def solve_online(plan: OnlinePlan, p, want_interval: bool = False) -> OnlineSolution:
+    """Solve the weighted subsampled least-squares problem at parameter p."""
+    res = solve_params(plan, [p])
+    _raise_for_status(res)
+    return _solution(plan, res, 0, want_interval)
+
+
+def estimate_residual(plan: OnlinePlan, solution: OnlineSolution):
+    """Heuristic residual interval (online.py:137-153)."""
+    sel = plan.selector
+    r = plan.basis.rank
+    if sel.weights is None:
+        raise ValueError("residual estimation requires a weighted selector")
+    if sel.size <= r:
+        raise ValueError("residual estimation requires oversampling (s > r)")
+    eps = min(max(r * math.log(r) / sel.size if r > 1 else 0.0, 0.0), 0.99)
+    est = solution.sampled_residual
+    return est, est / (1.0 + eps), est / (1.0 - eps), eps
+
+
+def solve_batch(plan: OnlinePlan, parameters, want_interval: bool = False, workers: int = 1) -> list:
+    """Solve many parameters; rows come back in input order.  One batched GPU
+    call; `workers` is accepted for API compatibility (the GPU batch replaces
+    the reference's thread pool, online.py:222-224).  wall_time is the batch
+    time divided evenly over its parameters."""
+    parameters = list(parameters)
+    if not parameters:
+        return []
+    res = solve_params(plan, parameters)
+    _raise_for_status(res)
+    per = res.seconds / len(parameters)
+    rows = []
+    for k, p in enumerate(parameters):
+        sol = _solution(plan, res, k, want_interval)
+        rows.append(BatchRow(parameter=p, sampled_residual=sol.sampled_residual,
+                             residual_interval=sol.residual_interval, output_value=sol.output_value,
+                             wall_time=per, solution=sol))
+    return rows
+
+
+def solve_apsnap(system, basis, p):
+    """Not on the online path: the full O(n r'^2) least squares stays in the
+    reference (online.py:156-165)."""
+    raise NotImplementedError("solve_apsnap is not part of the GPU online path; use subapsnap.online.solve_apsnap")
+
+
+# --------------------------------------------------------------------------
+# device-resident API (torch tensors; used by bench.py and the multi-GPU driver)
+# --------------------------------------------------------------------------
+def device_params(plan: OnlinePlan, parameters, device=None):
+    import torch
+    g = _gpu(plan)
+    arr = g.params_array(list(parameters))
+    return torch.from_numpy(arr).to(device or f"cuda:{g.device}")
+
+
+def alloc_outputs(plan: OnlinePlan, P: int, device=None):
+    import torch
+    g = _gpu(plan)
+    dev = device or f"cuda:{g.device}"
+    cdt = torch.complex128 if g.complex else torch.float64
+    return {
+        "coef": torch.empty((P, g.r), dtype=cdt, device=dev),
+        "sres": torch.empty(P, dtype=torch.float64, device=dev),
+        "outv": torch.empty((P, 2), dtype=torch.float64, device=dev),
+        "status": torch.empty(P, dtype=torch.int32, device=dev),
+        "bad": torch.empty(P, dtype=torch.int32, device=dev),
+    }
+
+
+def solve_device(plan: OnlinePlan, params_t, out: dict, stream=None, coef_table=None, rhs_table=None) -> int:
+    """Enqueue the batched solve on `stream` (torch stream; default: current).
+    All tensors live on the plan's device.  Returns the number of kernels
+    launched."""
+    import torch
+    g = _gpu(plan)
+    st = stream if stream is not None else torch.cuda.current_stream(g.device)
+    P = params_t.shape[0]
+    rc = g.lib.sas_solve(g.handle, _capi.ptr(params_t), P, _capi.ptr(coef_table), _capi.ptr(rhs_table),
+                         _capi.ptr(out["coef"]), _capi.ptr(out["sres"]), _capi.ptr(out["outv"]),
+                         _capi.ptr(out["status"]), _capi.ptr(out["bad"]), C.c_void_p(st.cuda_stream))
+    _capi.check(rc, "sas_solve")
+    return g.launches()
+
+
+def lift_batch(plan: OnlinePlan, coefficients) -> np.ndarray:
+    """x = Q_X c for a batch of coefficient vectors (P x r' -> P x n), on the GPU."""
+    import torch
+    g = _gpu(plan)
+    cf = np.ascontiguousarray(np.asarray(coefficients).astype(g.np_dtype))
+    P = cf.shape[0]
+    dev = f"cuda:{g.device}"
+    ct = torch.from_numpy(cf).to(dev)
+    x = torch.empty((P, g.n), dtype=ct.dtype, device=dev)
+    st = torch.cuda.current_stream(g.device)
+    _capi.check(g.lib.sas_lift(g.handle, _capi.ptr(ct), P, _capi.ptr(x), C.c_void_p(st.cuda_stream)), "sas_lift")
+    out = x.cpu().numpy()
+    return out.astype(g.result_dtype, copy=False)
+
+
+def set_full_operator(plan: OnlinePlan):
+    """Upload the full operator (for relative_residual)."""
+    g = _gpu(plan)
+    sysm = plan.system
+    b = np.ascontiguousarray(np.asarray(sysm.full_rhs(None) if g.rhs_constant else sysm.b).astype(g.np_dtype))
+    keep = [b]
+    op = getattr(sysm, "operator", None)
+    if sysm.affine_terms is not None:
+        K = len(sysm.affine_terms)
+        rps, cis, vas = (C.c_void_p * K)(), (C.c_void_p * K)(), (C.c_void_p * K)()
+        for k, t in enumerate(sysm.affine_terms):
+            m = t.matrix.tocsr()
+            rp = np.ascontiguousarray(m.indptr.astype(np.int64))
+            ci = np.ascontiguousarray(m.indices.astype(np.int64))
+            va = np.ascontiguousarray(m.data.astype(g.np_dtype))
+            keep += [rp, ci, va]
+            rps[k], cis[k], vas[k] = rp.ctypes.data, ci.ctypes.data, va.ctypes.data
+        rc = g.lib.sas_plan_set_operator(g.handle, rps, cis, vas, None, None, _capi.ptr(b))
+    elif isinstance(op, StencilOperator):
+        nbr, phi = op.edges(np.arange(op.n))
+        keep += [nbr, phi]
+        rc = g.lib.sas_plan_set_operator(g.handle, None, None, None, _capi.ptr(nbr), _capi.ptr(phi), _capi.ptr(b))
+    else:
+        rc = g.lib.sas_plan_set_operator(g.handle, None, None, None, None, None, _capi.ptr(b))
+    _capi.check(rc, "sas_plan_set_operator")
+    g._operator_set = True
+
+
+def relative_residual(plan: OnlinePlan, parameters, coefficients) -> np.ndarray:
+    """||A(p) Q_X c - b|| / max(||b||, 1e-300) per parameter (cli.py:285, 344-351), on the GPU."""
+    import torch
+    g = _gpu(plan)
+    if not g._operator_set:
+        set_full_operator(plan)
+    parameters = list(parameters)
+    dev = f"cuda:{g.device}"
+    pt = torch.from_numpy(g.params_array(parameters)).to(dev)
+    ct = torch.from_numpy(np.ascontiguousarray(np.asarray(coefficients).astype(g.np_dtype))).to(dev)
+    out = torch.empty(len(parameters), dtype=torch.float64, device=dev)
+    st = torch.cuda.current_stream(g.device)
+    _capi.check(g.lib.sas_residual(g.handle, _capi.ptr(pt), _capi.ptr(ct), len(parameters), _capi.ptr(out),
+                                   C.c_void_p(st.cuda_stream)), "sas_residual")
+    return out.cpu().numpy()
+
+
+# --------------------------------------------------------------------------
+# plan artifacts (online.py:168-195): same npz layout as the reference
+# --------------------------------------------------------------------------
+def save_plan(path, plan: OnlinePlan) -> None:
+    payload = {"sampled_basis": plan.sampled_basis, "affine": np.array(plan.affine)}
+    if plan.blocks is not None:
+        for k, blk in enumerate(plan.blocks):
+            payload[f"block_{k}"] = blk
+    if plan.output_projection is not None:
+        payload["output_projection"] = plan.output_projection
+    np.savez_compressed(path, **payload)
+
+
+def load_plan(path, system, basis, selector, device: int = 0) -> OnlinePlan:
+    data = np.load(path)
+    blocks = None
+    if bool(data["affine"]):
+        blocks = []
+        k = 0
+        while f"block_{k}" in data:
+            blocks.append(data[f"block_{k}"])
+            k += 1
+        blocks = tuple(blocks)
+    proj = data["output_projection"] if "output_projection" in data else None
+    gpu = GpuPlan(system, basis, selector, blocks, proj, device=device)
+    return OnlinePlan(system=system, basis=basis, selector=selector, blocks=blocks,
+                      sampled_basis=data["sampled_basis"], output_projection=proj, gpu=gpu)

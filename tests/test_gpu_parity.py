@@ -1,0 +1,148 @@
+"""Parity of the CUDA path (libsas.so through the drop-in API) with the
+reference's golden vectors and the CPU oracle, on seeded inputs.
+
+Tolerances (north_star): per-p coefficient relative difference
+<= max(1e-10, 10 * floor_p), floor_p = the spread of two valid fp64
+evaluations (tests/golden, oracle.online_ref.ls_floor); relative residual
+||A x - b|| / ||b|| to 3 significant digits when it is above its rounding
+floor 100 eps || |A| |x| || / ||b||, else both below that floor.
+"""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from _golden import GOLDEN_NAMES, full_matrix, load, oracle_solve
+from paper_2510_04825_b200 import online
+from paper_2510_04825_b200.errors import RankDeficiencyError
+
+pytestmark = pytest.mark.gpu
+
+EPS = np.finfo(float).eps
+
+
+def _tol(case, k):
+    return max(1e-10, 10.0 * float(case.data["floor"][k]))
+
+
+@pytest.fixture(scope="module", params=GOLDEN_NAMES)
+def solved(request):
+    case = load(request.param)
+    plan = online.precompute_online(case.system, case.basis, case.selector)
+    res = online.solve_params(plan, case.params)
+    return case, plan, res
+
+
+def test_coefficients_match_reference(solved):
+    case, plan, res = solved
+    assert np.all(res.status == 0)
+    ref = case.data["coef"]
+    for k in range(len(case.params)):
+        d = np.linalg.norm(res.coefficients[k] - ref[k]) / np.linalg.norm(ref[k])
+        assert d <= _tol(case, k), (case.name, k, d, case.data["floor"][k])
+
+
+def test_sampled_residual_matches_reference(solved):
+    case, plan, res = solved
+    ref = case.data["sres"]
+    for k in range(len(case.params)):
+        # the sampled residual inherits the coefficient error through M c - t;
+        # near the rounding floor it is noise, so compare absolutely there
+        scale = np.linalg.norm(case.selector.weights if case.selector.weights is not None else 1.0) * \
+            max(np.abs(case.data["coef"][k]).max(), 1.0)
+        assert abs(res.sampled_residual[k] - ref[k]) <= 1e-6 * ref[k] + 1e3 * EPS * scale * \
+            max(1.0, np.abs(oracle_solve(case, case.params[k])[0]).max()), (case.name, k)
+
+
+def test_output_value_matches_reference(solved):
+    case, plan, res = solved
+    if case.system.output_functional is None:
+        assert res.output_value is None
+        return
+    ref = case.data["outv"]
+    for k in range(len(case.params)):
+        assert abs(res.output_value[k] - ref[k]) <= max(1e-10, 10 * case.data["floor"][k]) * abs(ref[k]) + 1e-300
+
+
+def test_matches_oracle_on_all_params(solved):
+    case, plan, res = solved
+    for k in range(0, len(case.params), max(1, len(case.params) // 8)):
+        c, s, o = oracle_solve(case, case.params[k])
+        d = np.linalg.norm(res.coefficients[k] - c) / np.linalg.norm(c)
+        assert d <= _tol(case, k)
+
+
+def test_relative_residual_three_digits(solved):
+    case, plan, res = solved
+    if case.system.affine_terms is None and case.name == "cfg2":
+        ks = range(0, len(case.params), 16)  # n^2 exps per p: a subset
+    else:
+        ks = range(0, len(case.params), max(1, len(case.params) // 16))
+    ks = list(ks)
+    params = [case.params[k] for k in ks]
+    if not case.system.rhs_constant:
+        pytest.skip("p-dependent rhs: residual checker needs a constant b")
+    rr = online.relative_residual(plan, params, res.coefficients[ks])
+    for j, k in enumerate(ks):
+        p = case.params[k]
+        a = full_matrix(case, p)
+        x = case.basis.basis @ res.coefficients[k]
+        b = case.system.full_rhs(p)
+        absa = abs(a) if sp.issparse(a) else np.abs(a)
+        floor = 100 * EPS * np.linalg.norm(absa @ np.abs(x)) / np.linalg.norm(b)
+        ref = case.data["relres"][k]
+        if ref > floor:
+            assert rr[j] == pytest.approx(ref, rel=5e-4), (case.name, k, rr[j], ref, floor)
+        else:
+            assert rr[j] <= floor and ref <= floor
+
+
+def test_lift_matches_basis_product(solved):
+    case, plan, res = solved
+    x = online.lift_batch(plan, res.coefficients[:4])
+    ref = (case.basis.basis @ res.coefficients[:4].T).T
+    assert np.allclose(x, ref, rtol=1e-13, atol=1e-13 * np.abs(ref).max())
+
+
+def test_solve_batch_api_and_order(solved):
+    case, plan, res = solved
+    params = case.params[:7]
+    rows = online.solve_batch(plan, params, want_interval=True)
+    assert [r.parameter for r in rows] == params
+    for k, row in enumerate(rows):
+        assert np.array_equal(row.solution.coefficients, res.coefficients[k])
+        assert row.wall_time >= 0
+        if case.selector.weights is not None:
+            est, lo, hi, eps = online.estimate_residual(plan, row.solution)
+            assert row.residual_interval == (lo, hi)
+            assert lo <= est <= hi
+
+
+def test_rank_deficient_sampled_system_raises():
+    # test_online.py:147-156: the same row three times cannot determine 3 coefficients
+    case = load("tridiag_lupp")
+    from paper_2510_04825_b200.offline import RowSelector, SnapshotBasis
+    X = case.basis.basis[:, :3]
+    basis = SnapshotBasis(points=(), raw=X, basis=X, singular_values=np.ones(3))
+    sel = RowSelector(indices=[5, 5, 5], n=case.system.n, weights=np.array([1.0, 1.0, 1.0]))
+    plan = online.precompute_online(case.system, basis, sel)
+    with pytest.raises(RankDeficiencyError):
+        online.solve_online(plan, -9.5)
+
+
+def test_nonfinite_matrix_raises():
+    case = load("cfg1")
+    X = case.basis.basis.copy()
+    X[case.selector.indices[0], 0] = np.nan
+    from paper_2510_04825_b200.offline import SnapshotBasis
+    basis = SnapshotBasis(points=(), raw=X, basis=X, singular_values=np.ones(X.shape[1]))
+    plan = online.precompute_online(case.system, basis, case.selector)
+    with pytest.raises(ValueError, match="non-finite"):
+        online.solve_online(plan, 0.5)
+
+
+def test_empty_batch():
+    case = load("cfg1")
+    plan = online.precompute_online(case.system, case.basis, case.selector)
+    assert online.solve_batch(plan, []) == []
+    res = online.solve_params(plan, [])
+    assert res.coefficients.shape == (0, case.basis.rank)
