@@ -160,6 +160,15 @@ int sas_plan_info(const sas_plan* plan, int64_t* n, int32_t* r, int32_t* s,
 /* Number of kernels the last sas_solve enqueued (for launch accounting). */
 int32_t sas_last_launch_count(const sas_plan* plan);
 
+/* Per-launch timing.  With timing enabled, every kernel a call enqueues is
+ * bracketed by CUDA events on the launching stream; sas_stage_times
+ * synchronizes on them and returns, for the last sas_solve, the launch count
+ * and per-launch milliseconds with their stage ids (SAS_STAGE_*). */
+#define SAS_STAGE_LSQ 1        /* K4 batched least squares (+ fused assembly) */
+#define SAS_STAGE_GAUSS_ROWS 2 /* K3 Gaussian kernel-row contraction */
+int sas_plan_set_timing(sas_plan* plan, int32_t enable);
+int32_t sas_stage_times(sas_plan* plan, float* ms, int32_t* stage, int32_t cap);
+
 void sas_plan_destroy(sas_plan* plan);
 const char* sas_last_error(void);
 const char* sas_version(void);

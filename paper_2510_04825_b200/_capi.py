@@ -29,8 +29,9 @@ SAS_FLAG_INPUT_DEVICE = 1
 EXPORTS = (
     "sas_plan_create", "sas_solve", "sas_solve_host", "sas_lift", "sas_residual",
     "sas_plan_set_operator", "sas_plan_info", "sas_last_launch_count",
-    "sas_plan_destroy", "sas_last_error", "sas_version",
+    "sas_plan_destroy", "sas_last_error", "sas_version", "sas_plan_set_timing", "sas_stage_times",
 )
+SAS_STAGE_LSQ, SAS_STAGE_GAUSS_ROWS = 1, 2
 
 
 class SasDesc(C.Structure):
@@ -78,6 +79,10 @@ def _declare(lib):
     lib.sas_plan_info.restype = C.c_int
     lib.sas_last_launch_count.argtypes = [vp]
     lib.sas_last_launch_count.restype = C.c_int32
+    lib.sas_plan_set_timing.argtypes = [vp, i32]
+    lib.sas_plan_set_timing.restype = C.c_int
+    lib.sas_stage_times.argtypes = [vp, C.POINTER(C.c_float), C.POINTER(i32), i32]
+    lib.sas_stage_times.restype = C.c_int32
     lib.sas_plan_destroy.argtypes = [vp]
     lib.sas_plan_destroy.restype = None
     lib.sas_last_error.argtypes = []

@@ -137,6 +137,11 @@ struct sas_plan {
   int32_t* h_bad = nullptr; int64_t h_bad_n = 0;
   cudaStream_t stream = nullptr;
   int32_t last_launches = 0;
+  // per-launch CUDA-event timing (sas_plan_set_timing)
+  bool timing = false;
+  std::vector<cudaEvent_t> ev0, ev1;
+  std::vector<int32_t> ev_stage;
+  int nrec = 0;
   int sms = 148;
 };
 
@@ -198,6 +203,8 @@ static void plan_free(sas_plan* pl) {
   for (auto* p : pl->csr_ci) cudaFree(p);
   for (auto* p : pl->csr_va) cudaFree(p);
   if (pl->stream) cudaStreamDestroy(pl->stream);
+  for (auto e : pl->ev0) cudaEventDestroy(e);
+  for (auto e : pl->ev1) cudaEventDestroy(e);
   delete pl;
 }
 
@@ -368,6 +375,48 @@ extern "C" int sas_plan_info(const sas_plan* pl, int64_t* n, int32_t* r, int32_t
 
 extern "C" int32_t sas_last_launch_count(const sas_plan* pl) { return pl ? pl->last_launches : -1; }
 
+
+// ---------------------------------------------------------------------------
+// launch timing: events bracket every kernel the plan enqueues when enabled
+static void stage_begin(sas_plan* pl, cudaStream_t st, int32_t stage) {
+  if (!pl->timing) return;
+  if (pl->nrec >= (int)pl->ev0.size()) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    pl->ev0.push_back(a);
+    pl->ev1.push_back(b);
+    pl->ev_stage.push_back(0);
+  }
+  pl->ev_stage[pl->nrec] = stage;
+  cudaEventRecord(pl->ev0[pl->nrec], st);
+}
+static void stage_end(sas_plan* pl, cudaStream_t st) {
+  if (!pl->timing) return;
+  cudaEventRecord(pl->ev1[pl->nrec], st);
+  pl->nrec++;
+}
+
+extern "C" int sas_plan_set_timing(sas_plan* pl, int32_t enable) {
+  ARG_CHECK(pl, "null plan");
+  pl->timing = enable != 0;
+  pl->nrec = 0;
+  return SAS_OK;
+}
+
+extern "C" int32_t sas_stage_times(sas_plan* pl, float* ms, int32_t* stage, int32_t cap) {
+  if (!pl) return -1;
+  DevGuard g(pl->device);
+  int n = pl->nrec < cap ? pl->nrec : cap;
+  for (int i = 0; i < n; ++i) {
+    cudaEventSynchronize(pl->ev1[i]);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, pl->ev0[i], pl->ev1[i]);
+    if (ms) ms[i] = t;
+    if (stage) stage[i] = pl->ev_stage[i];
+  }
+  return n;
+}
 // ---------------------------------------------------------------------------
 // K4 launch: pick (NC, RPT) and the CTA size for (s, r).
 template <typename T, int NC, int RPT, class Asm>
@@ -387,7 +436,9 @@ static int launch_lsq_t(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t
   int64_t grid = (int64_t)occ * pl->sms;
   if (grid > a.P) grid = a.P;
   if (grid < 1) grid = 1;
+  stage_begin(pl, st, SAS_STAGE_LSQ);
   kern<<<(unsigned)grid, 32 * W, smem, st>>>(a, as, scratch);
+  stage_end(pl, st);
   SAS_CUDA_CHECK(cudaGetLastError());
   pl->last_launches++;
   return SAS_OK;
@@ -420,8 +471,10 @@ static int launch_gauss_nt(sas_plan* pl, const double* params, int64_t P, double
   auto kern = k_gauss_rows<NT, PW>;
   SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int64_t grid = (P + PW - 1) / PW;
+  stage_begin(pl, st, SAS_STAGE_GAUSS_ROWS);
   kern<<<(unsigned)grid, 32 * nw, smem, st>>>(pl->D, (const double*)pl->X, pl->S, params, P, pl->s, pl->n,
                                              pl->r, pl->ridge, Mout);
+  stage_end(pl, st);
   SAS_CUDA_CHECK(cudaGetLastError());
   pl->last_launches++;
   return SAS_OK;
@@ -518,6 +571,7 @@ extern "C" int sas_solve(sas_plan* pl, const void* params, int64_t P, const doub
   ARG_CHECK(pl, "null plan");
   ARG_CHECK(P >= 0, "P must be >= 0");
   pl->last_launches = 0;
+  pl->nrec = 0;
   if (P == 0) return SAS_OK;
   ARG_CHECK(params && coef && sres && status, "sas_solve: params, coef, sampled_res and status are required");
   DevGuard g(pl->device);

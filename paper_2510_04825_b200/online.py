@@ -204,6 +204,16 @@ class GpuPlan:
     def launches(self) -> int:
         return int(self.lib.sas_last_launch_count(self.handle))
 
+    def set_timing(self, enable: bool):
+        _capi.check(self.lib.sas_plan_set_timing(self.handle, 1 if enable else 0), "sas_plan_set_timing")
+
+    def stage_times(self, cap: int = 64):
+        """[(stage_id, ms)] for every kernel of the last solve (needs set_timing(True))."""
+        ms = (C.c_float * cap)()
+        st = (C.c_int32 * cap)()
+        n = self.lib.sas_stage_times(self.handle, ms, st, cap)
+        return [(int(st[i]), float(ms[i])) for i in range(max(n, 0))]
+
     def close(self):
         if getattr(self, "handle", None) is not None and self.handle.value:
             self.lib.sas_plan_destroy(self.handle)
