@@ -32,6 +32,8 @@ EXPORTS = (
     "sas_plan_destroy", "sas_last_error", "sas_version", "sas_plan_set_timing", "sas_stage_times",
 )
 SAS_STAGE_LSQ, SAS_STAGE_GAUSS_ROWS = 1, 2
+#: test-only symbols (include/sas_debug.h)
+DEBUG_EXPORTS = ("sas_debug_exp64_host", "sas_debug_exp64")
 
 
 class SasDesc(C.Structure):
@@ -91,6 +93,8 @@ def _declare(lib):
     lib.sas_version.restype = C.c_char_p
     lib.sas_debug_exp64_host.argtypes = [C.c_double]
     lib.sas_debug_exp64_host.restype = C.c_double
+    lib.sas_debug_exp64.argtypes = [vp, vp, i64, vp]
+    lib.sas_debug_exp64.restype = C.c_int
     return lib
 
 

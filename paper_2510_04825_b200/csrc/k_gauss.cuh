@@ -39,7 +39,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // D[i][l] = sum_k (x_{S_i,k} - x_{l,k})^2, sequential over k, no FMA
 // (the harness row oracle's order; see oracle/systems_ref.py gauss rows).
 __global__ void k_gauss_dist(const double* __restrict__ pts, const int64_t* __restrict__ S,
-                             int64_t n, int d, int s, double* __restrict__ D) {
+                             int64_t n, int d, int s, int64_t ld, double* __restrict__ D) {
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= (int64_t)s * n) return;
   int i = (int)(idx / n);
@@ -51,45 +51,77 @@ __global__ void k_gauss_dist(const double* __restrict__ pts, const int64_t* __re
     double df = __dsub_rn(xi[k], xl[k]);
     acc = __dadd_rn(acc, __dmul_rn(df, df));
   }
-  D[idx] = acc;
+  D[(int64_t)i * ld + l] = acc;
 }
 
 constexpr int kGaussKC = 32;            // K chunk staged per pipeline stage
-constexpr int kGaussLD = kGaussKC + 4;  // padded row stride (conflict-free fragments)
+constexpr int kGaussLD = kGaussKC + 4;  // padded smem row stride (conflict-free fragments)
+constexpr int kGaussStages = 3;         // cp.async pipeline depth
+constexpr int kGaussMaxWarps = 10;      // row groups (8 rows each) per CTA -> 320 threads
+// parameter values per CTA: keep PW*NT*2 accumulator doubles <= 24 (2 CTAs/SM)
+template <int NT>
+__host__ __device__ constexpr int gauss_pw() { return NT <= 3 ? 4 : (NT == 4 ? 3 : (NT <= 6 ? 2 : 1)); }
 
-template <int NT, int PW>
-__host__ __device__ constexpr size_t gauss_smem_bytes(int s_pad) {
-  return (size_t)2 * (s_pad + 8 * NT) * kGaussLD * sizeof(double);
+// Row blocking of the s selected rows: gy CTAs along grid.y with rows_cta rows each.
+__host__ __device__ inline void gauss_row_blocks(int s, int* gy, int* rows_cta) {
+  const int s_pad = ((s + 7) / 8) * 8;
+  *gy = (s_pad + 8 * kGaussMaxWarps - 1) / (8 * kGaussMaxWarps);
+  *rows_cta = 8 * ((s_pad / 8 + *gy - 1) / *gy);
 }
 
-// grid.x = ceil(P / PW); block = 32 * (s_pad / 8)
-template <int NT, int PW>
-__global__ void __launch_bounds__(384) k_gauss_rows(const double* __restrict__ D,   // s x n
-                                                    const double* __restrict__ X,   // n x r
-                                                    const int64_t* __restrict__ S,  // s
-                                                    const double* __restrict__ params,  // P
-                                                    int64_t P, int s, int64_t n, int r,
-                                                    double ridge,
-                                                    double* __restrict__ Mout) {  // P x s x r
+template <int NT>
+__host__ __device__ constexpr size_t gauss_smem_bytes(int rows_cta) {
+  return (size_t)kGaussStages * (rows_cta + 8 * NT) * kGaussLD * sizeof(double);
+}
+
+// Plan-time layouts (zero padded so the main loop needs no predicates):
+//   Dp  [gy*rows_cta][n_pad]  row blocks of rows_cta (gauss_row_blocks), n_pad = KC*ceil(n/KC)
+//   XT  [8*NT][n_pad]    X transposed, basis columns >= r are zero
+// Padding is exact: a padded l contributes exp(-0)*0 = 0, padded rows are not stored.
+__global__ void k_gauss_pack_xt(const double* __restrict__ X, int64_t n, int r, int64_t n_pad, int rows,
+                                double* __restrict__ XT) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)rows * n_pad) return;
+  int c = (int)(idx / n_pad);
+  int64_t l = idx - (int64_t)c * n_pad;
+  XT[idx] = (c < r && l < n) ? X[l * r + c] : 0.0;
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+
+// grid = (ceil(P / PW), ceil(s_pad / (8*kGaussMaxWarps))); block = 32 * (row groups of this block)
+template <int NT>
+__global__ void __launch_bounds__(32 * kGaussMaxWarps, 2)
+k_gauss_rows(const double* __restrict__ Dp,     // s_pad x n_pad
+             const double* __restrict__ XT,     // 8NT x n_pad
+             const int64_t* __restrict__ S,     // s
+             const double* __restrict__ params, // P
+             int64_t P, int s, int64_t n_pad, int r, double ridge,
+             double* __restrict__ Mout) {       // P x s x r
+  constexpr int PW = gauss_pw<NT>();
+  constexpr int XR = 8 * NT;
   extern __shared__ __align__(16) double gsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nwarps = blockDim.x >> 5;
-  const int s_pad = nwarps * 8;
-  const int XR = 8 * NT;
-  double* Ds[2] = {gsm, gsm + (size_t)(s_pad + XR) * kGaussLD};
-  double* Xs[2] = {gsm + (size_t)s_pad * kGaussLD, gsm + (size_t)(s_pad + XR) * kGaussLD + (size_t)s_pad * kGaussLD};
+  const int rows_cta = nwarps * 8;
+  const int row0 = blockIdx.y * rows_cta;  // first selected row of this CTA
+  const size_t stage_elems = (size_t)(rows_cta + XR) * kGaussLD;
 
   const int64_t pbase = (int64_t)blockIdx.x * PW;
-  double inv[PW];
+  double ninv[PW];
 #pragma unroll
   for (int u = 0; u < PW; ++u) {
-    int64_t p = pbase + u;
-    double sg = (p < P) ? params[p] : 1.0;
-    inv[u] = 1.0 / (2.0 * sg * sg);  // reference: inv = 1.0 / (2.0 * sigma * sigma)
+    const int64_t p = pbase + u;
+    const double sg = (p < P) ? params[p] : 1.0;
+    ninv[u] = -(1.0 / (2.0 * sg * sg));  // reference: inv = 1.0 / (2.0 * sigma * sigma)
   }
-  const int row = warp * 8 + (lane >> 2);   // A-fragment row = selected row i
-  const int kq = lane & 3;                  // A-fragment col within the k-step
-  const int64_t srow = (row < s) ? S[row] : -1;
+  const int lrow = warp * 8 + (lane >> 2);  // A-fragment row within the CTA
+  const int kq = lane & 3;                  // A-fragment column within the k-step
+  const int grow = row0 + lrow;
+  const int64_t srow = (grow < s) ? S[grow] : -1;
   const ExpTab tab = exp_tab_load(lane);
 
   double acc[PW][NT][2];
@@ -98,68 +130,67 @@ __global__ void __launch_bounds__(384) k_gauss_rows(const double* __restrict__ D
 #pragma unroll
     for (int t = 0; t < NT; ++t) acc[u][t][0] = acc[u][t][1] = 0.0;
 
-  const int64_t nchunks = (n + kGaussKC - 1) / kGaussKC;
+  const int64_t nchunks = n_pad / kGaussKC;
+  constexpr int kChunk16 = kGaussKC / 2;  // 16-byte pieces per row per stage
   auto stage = [&](int64_t ch, int b) {
+    double* base = gsm + (size_t)b * stage_elems;
     const int64_t l0 = ch * kGaussKC;
-    // D tile: s_pad x KC
-    for (int e = threadIdx.x; e < s_pad * kGaussKC; e += blockDim.x) {
-      int i = e / kGaussKC, kk = e - i * kGaussKC;
-      int64_t l = l0 + kk;
-      bool ok = (i < s) && (l < n);
-      cp_async8(&Ds[b][i * kGaussLD + kk], ok ? (const void*)(D + (int64_t)i * n + l) : (const void*)D, ok);
+    const int tot = (rows_cta + XR) * kChunk16;
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+      const int row = e / kChunk16, q = e - row * kChunk16;
+      const double* src = (row < rows_cta) ? Dp + (int64_t)(row0 + row) * n_pad + l0 + 2 * q
+                                           : XT + (int64_t)(row - rows_cta) * n_pad + l0 + 2 * q;
+      cp_async16(base + row * kGaussLD + 2 * q, src);
     }
-    // X tile transposed: Xs[col][kk]
-    for (int e = threadIdx.x; e < XR * kGaussKC; e += blockDim.x) {
-      int kk = e / XR, c = e - kk * XR;
-      int64_t l = l0 + kk;
-      bool ok = (c < r) && (l < n);
-      cp_async8(&Xs[b][c * kGaussLD + kk], ok ? (const void*)(X + l * r + c) : (const void*)X, ok);
-    }
-    cp_async_commit();
   };
 
-  stage(0, 0);
+#pragma unroll
+  for (int b = 0; b < kGaussStages - 1; ++b) {
+    if (b < nchunks) stage(b, b);
+    cp_async_commit();
+  }
   for (int64_t ch = 0; ch < nchunks; ++ch) {
-    const int b = (int)(ch & 1);
-    if (ch + 1 < nchunks) {
-      stage(ch + 1, b ^ 1);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    cp_async_wait<kGaussStages - 2>();
     __syncthreads();
-    const double* dsb = Ds[b];
-    const double* xsb = Xs[b];
+    {
+      const int64_t nx = ch + kGaussStages - 1;
+      if (nx < nchunks) stage(nx, (int)(nx % kGaussStages));
+      cp_async_commit();
+    }
+    const double* dsb = gsm + (size_t)(ch % kGaussStages) * stage_elems;
+    const double* xsb = dsb + (size_t)rows_cta * kGaussLD;
     const int64_t l0 = ch * kGaussKC;
-#pragma unroll 2
+    const int dcol = (srow >= l0 && srow < l0 + kGaussKC) ? (int)(srow - l0) : -1;
+#pragma unroll 1
     for (int kk = 0; kk < kGaussKC; kk += 4) {
-      const double dv = dsb[row * kGaussLD + kk + kq];
+      const double dv = dsb[lrow * kGaussLD + kk + kq];
       double bf[NT];
 #pragma unroll
       for (int t = 0; t < NT; ++t) bf[t] = xsb[(t * 8 + (lane >> 2)) * kGaussLD + kk + kq];
-      const bool diag = (l0 + kk + kq) == srow;
+      const bool diag = (kk + kq) == dcol;
 #pragma unroll
       for (int u = 0; u < PW; ++u) {
-        double e = sas_exp64(-(dv * inv[u]), tab);
+        double e = sas_exp64(dv * ninv[u], tab);
         if (diag) e = e + ridge;
 #pragma unroll
         for (int t = 0; t < NT; ++t) dmma884(acc[u][t][0], acc[u][t][1], e, bf[t]);
       }
     }
-    __syncthreads();
   }
+  cp_async_wait<0>();
   // C fragment: lane holds C[lane/4][2*(lane%4) + {0,1}]
-  const int crow = warp * 8 + (lane >> 2);
+  if (grow < s) {
 #pragma unroll
-  for (int u = 0; u < PW; ++u) {
-    const int64_t p = pbase + u;
-    if (p >= P || crow >= s) continue;
-    double* out = Mout + (p * s + crow) * (int64_t)r;
+    for (int u = 0; u < PW; ++u) {
+      const int64_t p = pbase + u;
+      if (p >= P) continue;
+      double* out = Mout + (p * s + grow) * (int64_t)r;
 #pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      const int c0 = t * 8 + 2 * (lane & 3);
-      if (c0 < r) out[c0] = acc[u][t][0];
-      if (c0 + 1 < r) out[c0 + 1] = acc[u][t][1];
+      for (int t = 0; t < NT; ++t) {
+        const int c0 = t * 8 + 2 * (lane & 3);
+        if (c0 < r) out[c0] = acc[u][t][0];
+        if (c0 + 1 < r) out[c0 + 1] = acc[u][t][1];
+      }
     }
   }
 }

@@ -109,7 +109,9 @@ struct sas_plan {
   double* pts = nullptr;
   int pdim = 0;
   double ridge = 0.0;
-  double* D = nullptr;
+  double* D = nullptr;   // s_pad x n_pad squared distances (zero padded)
+  double* XT = nullptr;  // 8*ceil(r/8) x n_pad transposed basis (zero padded)
+  int64_t n_pad = 0;
   // full operator for the residual checker
   int64_t* full_nbr = nullptr;
   double* full_phi = nullptr;
@@ -193,7 +195,7 @@ static void plan_free(sas_plan* pl) {
   if (!pl) return;
   DevGuard g(pl->device);
   void* ptrs[] = {pl->X, pl->S, pl->w, pl->t, pl->proj, pl->kind, pl->scale, pl->rate, pl->blocks,
-                  pl->phi, pl->G, pl->pts, pl->D, pl->full_nbr, pl->full_phi, pl->full_b,
+                  pl->phi, pl->G, pl->pts, pl->D, pl->XT, pl->full_nbr, pl->full_phi, pl->full_b,
                   pl->csr_rp_d, pl->csr_ci_d, pl->csr_va_d, pl->Mscr, pl->rpart, pl->fco,
                   pl->h_params, pl->h_ctab, pl->h_rhs, pl->h_coef, pl->h_sres, pl->h_outv,
                   pl->h_status, pl->h_bad};
@@ -225,6 +227,23 @@ extern "C" const char* sas_last_error(void) { return g_err.c_str(); }
 extern "C" const char* sas_version(void) { return "sas 0.1.0 (sm_100a)"; }
 extern "C" double sas_debug_exp64_host(double x) { return sas_exp64_host(x); }
 
+__global__ void k_debug_exp64(const double* x, double* y, int64_t n) {
+  const ExpTab tab = exp_tab_load(threadIdx.x & 31);
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const double v = sas_exp64(i < n ? x[i] : 0.0, tab);  // all lanes take part in the shuffles
+    if (i < n) y[i] = v;
+  }
+}
+
+// Device evaluation of the kernel-row exp (sas_exp64) for accuracy tests; device pointers.
+extern "C" int sas_debug_exp64(const double* x, double* y, int64_t n, void* stream) {
+  if (n <= 0) return SAS_OK;
+  k_debug_exp64<<<256, 256, 0, (cudaStream_t)stream>>>(x, y, n);
+  SAS_CUDA_CHECK(cudaGetLastError());
+  return SAS_OK;
+}
+
 extern "C" int sas_plan_create(const sas_desc* desc, const void* X, int64_t n, int32_t r,
                                const int64_t* S, const double* w, int32_t s, const void* t,
                                const void* proj, int32_t device, uint32_t flags, sas_plan** out) {
@@ -254,8 +273,7 @@ extern "C" int sas_plan_create(const sas_desc* desc, const void* X, int64_t n, i
   } else if (desc->op_kind == SAS_OP_GAUSS) {
     ARG_CHECK(desc->dtype == SAS_F64 && !desc->param_complex && desc->param_dim == 1, "gauss: real scalar bandwidth only");
     ARG_CHECK(desc->points && desc->point_dim >= 1, "gauss: points required");
-    ARG_CHECK(s <= 96, "gauss: s <= 96");
-  } else {
+      } else {
     ARG_CHECK(false, "unknown op_kind %d", desc->op_kind);
   }
 
@@ -340,11 +358,20 @@ extern "C" int sas_plan_create(const sas_desc* desc, const void* X, int64_t n, i
       pl->pdim = desc->point_dim;
       pl->ridge = desc->ridge;
       TRY(dupload(&pl->pts, desc->points, (size_t)n * pl->pdim * sizeof(double)));
-      TRY(dalloc(&pl->D, (size_t)s * n * sizeof(double)));
+      int gy, rows_cta;
+      gauss_row_blocks(s, &gy, &rows_cta);
+      const int s_pad = gy * rows_cta;
+      const int xr = 8 * ((r + 7) / 8);
+      pl->n_pad = ((n + kGaussKC - 1) / kGaussKC) * kGaussKC;
+      TRY(dalloc(&pl->D, (size_t)s_pad * pl->n_pad * sizeof(double)));
+      TRY(dalloc(&pl->XT, (size_t)xr * pl->n_pad * sizeof(double)));
+      cudaMemset(pl->D, 0, (size_t)s_pad * pl->n_pad * sizeof(double));
       int64_t tot = (int64_t)s * n;
-      k_gauss_dist<<<(unsigned)((tot + 255) / 256), 256>>>(pl->pts, pl->S, n, pl->pdim, s, pl->D);
+      k_gauss_dist<<<(unsigned)((tot + 255) / 256), 256>>>(pl->pts, pl->S, n, pl->pdim, s, pl->n_pad, pl->D);
+      int64_t totx = (int64_t)xr * pl->n_pad;
+      k_gauss_pack_xt<<<(unsigned)((totx + 255) / 256), 256>>>((const double*)pl->X, n, r, pl->n_pad, xr, pl->XT);
       cudaError_t e = cudaDeviceSynchronize();
-      if (e != cudaSuccess) { plan_free(pl); sas_set_error("gauss dist: %s", cudaGetErrorString(e)); return SAS_ERR_CUDA; }
+      if (e != cudaSuccess) { plan_free(pl); sas_set_error("gauss plan: %s", cudaGetErrorString(e)); return SAS_ERR_CUDA; }
       break;
     }
     default:
@@ -461,19 +488,15 @@ static int launch_lsq(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t s
 // K3 launch
 template <int NT>
 static int launch_gauss_nt(sas_plan* pl, const double* params, int64_t P, double* Mout, cudaStream_t st) {
-  constexpr int PW = 4;
-  const int nw = (pl->s + 7) / 8;
-  if (nw > 12) {
-    sas_set_error("gauss rows: s=%d > 96 not supported", pl->s);
-    return SAS_ERR_ARG;
-  }
-  const size_t smem = gauss_smem_bytes<NT, PW>(nw * 8);
-  auto kern = k_gauss_rows<NT, PW>;
+  int gy, rows_cta;
+  gauss_row_blocks(pl->s, &gy, &rows_cta);
+  const int nw = rows_cta / 8;
+  const size_t smem = gauss_smem_bytes<NT>(nw * 8);
+  auto kern = k_gauss_rows<NT>;
   SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int64_t grid = (P + PW - 1) / PW;
+  dim3 grid((unsigned)((P + gauss_pw<NT>() - 1) / gauss_pw<NT>()), (unsigned)gy);
   stage_begin(pl, st, SAS_STAGE_GAUSS_ROWS);
-  kern<<<(unsigned)grid, 32 * nw, smem, st>>>(pl->D, (const double*)pl->X, pl->S, params, P, pl->s, pl->n,
-                                             pl->r, pl->ridge, Mout);
+  kern<<<grid, 32 * nw, smem, st>>>(pl->D, pl->XT, pl->S, params, P, pl->s, pl->n_pad, pl->r, pl->ridge, Mout);
   stage_end(pl, st);
   SAS_CUDA_CHECK(cudaGetLastError());
   pl->last_launches++;
@@ -481,8 +504,7 @@ static int launch_gauss_nt(sas_plan* pl, const double* params, int64_t P, double
 }
 
 static int launch_gauss(sas_plan* pl, const double* params, int64_t P, double* Mout, cudaStream_t st) {
-  const int nt = (pl->r + 7) / 8;
-  switch (nt) {
+  switch ((pl->r + 7) / 8) {
     case 1: return launch_gauss_nt<1>(pl, params, P, Mout, st);
     case 2: return launch_gauss_nt<2>(pl, params, P, Mout, st);
     case 3: return launch_gauss_nt<3>(pl, params, P, Mout, st);

@@ -1,0 +1,63 @@
+"""Kernel-level GPU checks: the K3 exponential, the Gaussian row blocking for
+s > 80, full-size config-2 properties, multi-chunk launches."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import online_ref
+from paper_2510_04825_b200 import _capi, online, problems
+from paper_2510_04825_b200.offline import offline
+
+pytestmark = pytest.mark.gpu
+
+
+def test_device_exp_ulp():
+    import torch
+    lib = _capi.load()
+    rng = np.random.default_rng(1)
+    xs = np.concatenate([-rng.uniform(0, 40, 200_000), -rng.uniform(0, 708, 50_000), [0.0, -1e-300, -708.3]])
+    x = torch.from_numpy(xs).cuda()
+    y = torch.empty_like(x)
+    _capi.check(lib.sas_debug_exp64(_capi.ptr(x), _capi.ptr(y), x.numel(),
+                                    C.c_void_p(torch.cuda.current_stream().cuda_stream)), "exp")
+    got = y.cpu().numpy()
+    ref = np.exp(xs)
+    ulp = np.abs(got - ref) / np.spacing(ref)
+    assert ulp.max() <= 2.0
+    host = np.array([lib.sas_debug_exp64_host(float(v)) for v in xs[:2000]])
+    assert np.array_equal(host, got[:2000])  # same algorithm bit for bit
+
+
+def _gauss_case(n, s, seed=0, count=24):
+    prob = problems.gauss_krr(n=n, seed=seed)
+    prob.samples = s
+    basis, sel = offline(prob)
+    return prob, basis, sel, prob.test_params(count)
+
+
+@pytest.mark.parametrize("n,s", [(700, 96), (517, 40), (2048, 80)])
+def test_gauss_rows_match_oracle(n, s):
+    prob, basis, sel, params = _gauss_case(n, s)
+    plan = online.precompute_online(prob.system, basis, sel)
+    res = online.solve_params(plan, params)
+    assert np.all(res.status == 0)
+    op = prob.system.operator
+    fn = lambda q, rows: online_ref.gauss_rows(op.points, rows, float(q), op.ridge)
+    for k, p in enumerate(params):
+        m = online_ref.sampled_rows(fn, basis.basis, sel.indices, p)
+        c, sres, _ = online_ref.solve_one(m, prob.system.rhs(p, sel.indices), sel.weights)
+        floor = online_ref.ls_floor(m, prob.system.rhs(p, sel.indices), sel.weights)
+        d = np.linalg.norm(res.coefficients[k] - c) / np.linalg.norm(c)
+        assert d <= max(1e-10, 10 * floor), (k, d, floor)
+
+
+def test_batch_sizes_and_order_independence():
+    # results for a parameter do not depend on the batch it is solved in
+    prob, basis, sel, params = _gauss_case(1000, 80, count=37)
+    plan = online.precompute_online(prob.system, basis, sel)
+    full = online.solve_params(plan, params)
+    part = online.solve_params(plan, params[5:18])
+    assert np.array_equal(full.coefficients[5:18], part.coefficients)
+    rev = online.solve_params(plan, params[::-1])
+    assert np.array_equal(full.coefficients, rev.coefficients[::-1])
