@@ -71,7 +71,7 @@ __host__ __device__ inline void gauss_row_blocks(int s, int* gy, int* rows_cta) 
 
 template <int NT>
 __host__ __device__ constexpr size_t gauss_smem_bytes(int rows_cta) {
-  return (size_t)kGaussStages * (rows_cta + 8 * NT) * kGaussLD * sizeof(double);
+  return (size_t)kGaussStages * (rows_cta + 8 * NT) * kGaussLD * sizeof(double) + 2048 * sizeof(double);
 }
 
 // Plan-time layouts (zero padded so the main loop needs no predicates):
@@ -93,15 +93,14 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 
 // grid = (ceil(P / PW), ceil(s_pad / (8*kGaussMaxWarps))); block = 32 * (row groups of this block)
-template <int NT>
-__global__ void __launch_bounds__(32 * kGaussMaxWarps, 2)
+template <int NT, int PW, int MINB, bool SMEM_TAB>
+__global__ void __launch_bounds__(32 * kGaussMaxWarps, MINB)
 k_gauss_rows(const double* __restrict__ Dp,     // s_pad x n_pad
              const double* __restrict__ XT,     // 8NT x n_pad
              const int64_t* __restrict__ S,     // s
              const double* __restrict__ params, // P
              int64_t P, int s, int64_t n_pad, int r, double ridge,
              double* __restrict__ Mout) {       // P x s x r
-  constexpr int PW = gauss_pw<NT>();
   constexpr int XR = 8 * NT;
   extern __shared__ __align__(16) double gsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -122,7 +121,11 @@ k_gauss_rows(const double* __restrict__ Dp,     // s_pad x n_pad
   const int kq = lane & 3;                  // A-fragment column within the k-step
   const int grow = row0 + lrow;
   const int64_t srow = (grow < s) ? S[grow] : -1;
-  const ExpTab tab = exp_tab_load(lane);
+  double* tab_s = gsm + (size_t)kGaussStages * stage_elems;
+  if (SMEM_TAB)
+    for (int j = threadIdx.x; j < 2048; j += blockDim.x) tab_s[j] = g_exp2_tab2048[j];
+  ExpTab tab{0.0, 0.0};
+  if (!SMEM_TAB) tab = exp_tab_load(lane);
 
   double acc[PW][NT][2];
 #pragma unroll
@@ -170,7 +173,7 @@ k_gauss_rows(const double* __restrict__ Dp,     // s_pad x n_pad
       const bool diag = (kk + kq) == dcol;
 #pragma unroll
       for (int u = 0; u < PW; ++u) {
-        double e = sas_exp64(dv * ninv[u], tab);
+        double e = SMEM_TAB ? sas_exp64_t2k(dv * ninv[u], tab_s) : sas_exp64(dv * ninv[u], tab);
         if (diag) e = e + ridge;
 #pragma unroll
         for (int t = 0; t < NT; ++t) dmma884(acc[u][t][0], acc[u][t][1], e, bf[t]);

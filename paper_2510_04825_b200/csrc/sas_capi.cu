@@ -19,6 +19,10 @@
 #include "k_gauss.cuh"
 #include "k_recon.cuh"
 
+static const double h_exp2_tab2048[2048] = {
+#include "exp2_table2048.inc"
+};
+
 static const double h_exp2_tab64[64] = {
     0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
     0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0,
@@ -57,28 +61,26 @@ void sas_set_error(const char* fmt, ...) {
     }                               \
   } while (0)
 
+// Host mirror of sas_exp64_t2k (the K3 exponential), bit for bit.
 double sas_exp64_host(double x) {
-  volatile double kd = fma(x, SAS_INVLN2X64, SAS_EXP_MAGIC);
-  int64_t bits;
+  volatile double kd = fma(x, SAS_INVLN2X2K, SAS_EXP_MAGIC);
   double kdv = kd;
+  int64_t bits;
   memcpy(&bits, &kdv, 8);
-  int ki = (int)(uint32_t)(bits & 0xffffffffu);
-  double kf = kdv - SAS_EXP_MAGIC;
-  double r = fma(-kf, SAS_LN2D64_HI, x);
-  r = fma(-kf, SAS_LN2D64_LO, r);
-  double q = fma(r, 1.0 / 120.0, 1.0 / 24.0);
-  q = fma(q, r, 1.0 / 6.0);
-  q = fma(q, r, 0.5);
+  const int ki = (int)(uint32_t)(bits & 0xffffffffu);
+  const double kf = kdv - SAS_EXP_MAGIC;
+  double r = fma(-kf, SAS_LN2D2K_HI, x);
+  r = fma(-kf, SAS_LN2D2K_LO, r);
+  double q = fma(r, 1.0 / 6.0, 0.5);
   q = fma(q, r, 1.0);
   q = q * r;
-  double t = h_exp2_tab64[ki & 63];
+  const double t = h_exp2_tab2048[ki & 2047];
   double res = fma(t, q, t);
-  int e = ki >> 6;
   int64_t rb;
   memcpy(&rb, &res, 8);
-  rb += (int64_t)e << 52;
+  rb += (int64_t)(ki >> 11) << 52;
   memcpy(&res, &rb, 8);
-  return (x < -708.39) ? 0.0 : res;
+  return (ki >= SAS_EXP2K_KMIN) ? res : 0.0;
 }
 
 // ---------------------------------------------------------------------------
@@ -228,12 +230,11 @@ extern "C" const char* sas_version(void) { return "sas 0.1.0 (sm_100a)"; }
 extern "C" double sas_debug_exp64_host(double x) { return sas_exp64_host(x); }
 
 __global__ void k_debug_exp64(const double* x, double* y, int64_t n) {
-  const ExpTab tab = exp_tab_load(threadIdx.x & 31);
-  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = base + threadIdx.x;
-    const double v = sas_exp64(i < n ? x[i] : 0.0, tab);  // all lanes take part in the shuffles
-    if (i < n) y[i] = v;
-  }
+  __shared__ double tab_s[2048];
+  for (int j = threadIdx.x; j < 2048; j += blockDim.x) tab_s[j] = g_exp2_tab2048[j];
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = sas_exp64_t2k(x[i], tab_s);
 }
 
 // Device evaluation of the kernel-row exp (sas_exp64) for accuracy tests; device pointers.
@@ -485,22 +486,52 @@ static int launch_lsq(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t s
   return launch_lsq_t<T, 2, 16>(pl, a, as, scratch, st);
 }
 
-// K3 launch
-template <int NT>
-static int launch_gauss_nt(sas_plan* pl, const double* params, int64_t P, double* Mout, cudaStream_t st) {
+// K3 launch.  Variant (PW, min blocks/SM, exp table in smem) chosen per NT;
+// SAS_K3_VARIANT=<pw>,<minb>,<smemtab> overrides it for tuning runs.
+template <int NT, int PW, int MINB, bool TAB>
+static int launch_gauss_v(sas_plan* pl, const double* params, int64_t P, double* Mout, cudaStream_t st) {
   int gy, rows_cta;
   gauss_row_blocks(pl->s, &gy, &rows_cta);
   const int nw = rows_cta / 8;
   const size_t smem = gauss_smem_bytes<NT>(nw * 8);
-  auto kern = k_gauss_rows<NT>;
+  auto kern = k_gauss_rows<NT, PW, MINB, TAB>;
   SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((unsigned)((P + gauss_pw<NT>() - 1) / gauss_pw<NT>()), (unsigned)gy);
+  dim3 grid((unsigned)((P + PW - 1) / PW), (unsigned)gy);
   stage_begin(pl, st, SAS_STAGE_GAUSS_ROWS);
   kern<<<grid, 32 * nw, smem, st>>>(pl->D, pl->XT, pl->S, params, P, pl->s, pl->n_pad, pl->r, pl->ridge, Mout);
   stage_end(pl, st);
   SAS_CUDA_CHECK(cudaGetLastError());
   pl->last_launches++;
   return SAS_OK;
+}
+
+static int k3_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SAS_K3_VARIANT");
+    v = 0;
+    if (e) {
+      int pw = 0, mb = 0, tb = 0;
+      if (sscanf(e, "%d,%d,%d", &pw, &mb, &tb) == 3) v = pw * 100 + mb * 10 + tb;
+    }
+  }
+  return v;
+}
+
+template <int NT>
+static int launch_gauss_nt(sas_plan* pl, const double* params, int64_t P, double* Mout, cudaStream_t st) {
+  if constexpr (NT == 3) {
+    switch (k3_variant()) {
+      case 421: return launch_gauss_v<3, 4, 2, true>(pl, params, P, Mout, st);
+      case 420: return launch_gauss_v<3, 4, 2, false>(pl, params, P, Mout, st);
+      case 231: return launch_gauss_v<3, 2, 3, true>(pl, params, P, Mout, st);
+      case 230: return launch_gauss_v<3, 2, 3, false>(pl, params, P, Mout, st);
+      case 321: return launch_gauss_v<3, 3, 2, true>(pl, params, P, Mout, st);
+      case 221: return launch_gauss_v<3, 2, 2, true>(pl, params, P, Mout, st);
+      default: break;
+    }
+  }
+  return launch_gauss_v<NT, gauss_pw<NT>(), 2, true>(pl, params, P, Mout, st);
 }
 
 static int launch_gauss(sas_plan* pl, const double* params, int64_t P, double* Mout, cudaStream_t st) {

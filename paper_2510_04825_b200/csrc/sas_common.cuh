@@ -149,6 +149,11 @@ struct Sc<cplx> {
 #define SAS_INVLN2X64 0x1.71547652b82fep+6
 #define SAS_EXP_MAGIC 0x1.8p52
 
+// 2^(j/2048), j = 0..2047 (correctly rounded), copied to shared memory by K3.
+__device__ const double g_exp2_tab2048[2048] = {
+#include "exp2_table2048.inc"
+};
+
 // 2^(j/64), j = 0..63 (correctly rounded; libsas is a single translation unit).
 __constant__ double c_exp2_tab64[64] = {
     0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
@@ -178,10 +183,11 @@ __device__ __forceinline__ ExpTab exp_tab_load(int lane) {
   return ExpTab{c_exp2_tab64[lane], c_exp2_tab64[lane + 32]};
 }
 
-// All 32 lanes of the warp must call this together (warp shuffles).
-__device__ __forceinline__ double sas_exp64(double x, const ExpTab& tab) {
+// Shared pieces of the exp: range reduction + polynomial, and the final scaling.
+// Returns q = e^r - 1 and k.
+__device__ __forceinline__ double sas_exp64_core(double x, int& ki) {
   double kd = fma(x, SAS_INVLN2X64, SAS_EXP_MAGIC);
-  int ki = __double2loint(kd);
+  ki = __double2loint(kd);
   double kf = kd - SAS_EXP_MAGIC;
   double r = fma(-kf, SAS_LN2D64_HI, x);
   r = fma(-kf, SAS_LN2D64_LO, r);
@@ -190,16 +196,62 @@ __device__ __forceinline__ double sas_exp64(double x, const ExpTab& tab) {
   q = fma(q, r, 1.0 / 6.0);
   q = fma(q, r, 0.5);
   q = fma(q, r, 1.0);
-  q = q * r;
-  int j = ki & 63;
-  double tlo = __shfl_sync(0xffffffffu, tab.lo, j & 31);
-  double thi = __shfl_sync(0xffffffffu, tab.hi, j & 31);
-  double t = (j & 32) ? thi : tlo;
+  return q * r;
+}
+
+// res = t (1 + q) scaled by 2^(k div 64); k < -65407 (x < -708.39, true value
+// subnormal) flushes to +0 with integer ops only (no FP64-pipe compare).
+__device__ __forceinline__ double sas_exp64_finish(double t, double q, int ki) {
   double res = fma(t, q, t);  // in [0.99, 2.01)
   int e = ki >> 6;            // floor(k / 64)
   int hi = __double2hiint(res) + (e << 20);
-  res = __hiloint2double(hi, __double2loint(res));
-  return (x < -708.39) ? 0.0 : res;
+  int lo = __double2loint(res);
+  const int keep = (ki >= -65407) ? -1 : 0;
+  return __hiloint2double(hi & keep, lo & keep);
+}
+
+// All 32 lanes of the warp must call this together (warp shuffles).
+__device__ __forceinline__ double sas_exp64(double x, const ExpTab& tab) {
+  int ki;
+  const double q = sas_exp64_core(x, ki);
+  const int j = ki & 63;
+  const double tlo = __shfl_sync(0xffffffffu, tab.lo, j & 31);
+  const double thi = __shfl_sync(0xffffffffu, tab.hi, j & 31);
+  return sas_exp64_finish((j & 32) ? thi : tlo, q, ki);
+}
+
+// Same algorithm with the 2^(j/64) table in shared memory (no warp collectives).
+__device__ __forceinline__ double sas_exp64_smem(double x, const double* __restrict__ tab_s) {
+  int ki;
+  const double q = sas_exp64_core(x, ki);
+  return sas_exp64_finish(tab_s[ki & 63], q, ki);
+}
+
+// K3 variant: 2048-entry table in shared memory, degree-3 polynomial.
+//   k = rint(x 2048/ln2), r = x - k ln2/2048 (two-constant, |r| <= ln2/4096),
+//   e^r - 1 = r (1 + r/2 + r^2/6) (truncation r^4/24 <= 3.4e-17),
+//   e^x = 2^(k mod 2048 / 2048) (1 + q) 2^(k div 2048).
+// 9 FP64-pipe ops per value (the 64-entry version needs 11).  k < -2093055
+// (x < -708.39) flushes to +0.
+#define SAS_INVLN2X2K 0x1.71547652b82fep+11
+#define SAS_LN2D2K_HI 0x1.62e42fec00000p-12
+#define SAS_LN2D2K_LO 0x1.d1cf79abc9e3bp-43
+#define SAS_EXP2K_KMIN (-2093055)
+
+__device__ __forceinline__ double sas_exp64_t2k(double x, const double* __restrict__ tab_s) {
+  const double kd = fma(x, SAS_INVLN2X2K, SAS_EXP_MAGIC);
+  const int ki = __double2loint(kd);
+  const double kf = kd - SAS_EXP_MAGIC;
+  double r = fma(-kf, SAS_LN2D2K_HI, x);
+  r = fma(-kf, SAS_LN2D2K_LO, r);
+  double q = fma(r, 1.0 / 6.0, 0.5);
+  q = fma(q, r, 1.0);
+  q = q * r;
+  const double t = tab_s[ki & 2047];
+  const double res = fma(t, q, t);
+  const int hi = __double2hiint(res) + ((ki >> 11) << 20);
+  const int keep = (ki >= SAS_EXP2K_KMIN) ? -1 : 0;
+  return __hiloint2double(hi & keep, __double2loint(res) & keep);
 }
 
 // Host reference of the same algorithm (for the CPU accuracy test).
