@@ -16,8 +16,10 @@
 // for PW parameters; per k-step of 4 each lane evaluates PW exps (A-fragment
 // element of mma.m8n8k4: row lane/4, col lane%4) and issues PW*NT DMMA
 // (mma.sync.m8n8k4.f64, SASS DMMA.8x8x4 — the only FP64 tensor shape on sm_100a;
-// FP64 has no tcgen05 kind).  D and X tiles are staged in shared memory with
-// cp.async (double-buffered) and reused by all PW parameters of the CTA.
+// FP64 has no tcgen05 kind).  D and X fragments stream through a 3-stage
+// shared-memory ring filled by bulk async copies (below) and are reused by all
+// PW parameters of the CTA.  The exp is sas_exp64_t2k (9 FP64-pipe ops; DMMA
+// and DFMA share one FP64 pipe on B200, profiles/r01_fp64_peaks.jsonl).
 #pragma once
 #include "sas_common.cuh"
 
@@ -27,17 +29,8 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
-  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  int sz = pred ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
 // D[i][l] = sum_k (x_{S_i,k} - x_{l,k})^2, sequential over k, no FMA
-// (the harness row oracle's order; see oracle/systems_ref.py gauss rows).
+// (the harness row oracle's order, oracle/online_ref.py gauss_rows).
 __global__ void k_gauss_dist(const double* __restrict__ pts, const int64_t* __restrict__ S,
                              int64_t n, int d, int s, int64_t ld, double* __restrict__ D) {
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -54,9 +47,7 @@ __global__ void k_gauss_dist(const double* __restrict__ pts, const int64_t* __re
   D[(int64_t)i * ld + l] = acc;
 }
 
-constexpr int kGaussKC = 32;            // K chunk staged per pipeline stage
-constexpr int kGaussLD = kGaussKC + 4;  // padded smem row stride (conflict-free fragments)
-constexpr int kGaussStages = 3;         // cp.async pipeline depth
+constexpr int kGaussKC = 32;            // K chunk (columns l) per pipeline stage
 constexpr int kGaussMaxWarps = 10;      // row groups (8 rows each) per CTA -> 320 threads
 // parameter values per CTA: keep PW*NT*2 accumulator doubles <= 24 (2 CTAs/SM)
 template <int NT>
@@ -69,45 +60,126 @@ __host__ __device__ inline void gauss_row_blocks(int s, int* gy, int* rows_cta) 
   *rows_cta = 8 * ((s_pad / 8 + *gy - 1) / *gy);
 }
 
-template <int NT>
-__host__ __device__ constexpr size_t gauss_smem_bytes(int rows_cta) {
-  return (size_t)kGaussStages * (rows_cta + 8 * NT) * kGaussLD * sizeof(double) + 2048 * sizeof(double);
-}
+// ===========================================================================
+// Fragment-ordered operands streamed with bulk async copies.
+//
+// Plan-time layouts put every DMMA fragment a warp needs for one k-step in 32
+// consecutive doubles (lane order), so a pipeline stage is two contiguous
+// blocks (the CTA's D fragments and the X^T fragments of one K chunk):
+//   Dfrag[rb][ch][g][ks][lane] = D[rb*rows_cta + 8g + lane/4][ch*KC + 4ks + lane%4]
+//   Xfrag[ch][t][ks][lane]     = X[ch*KC + 4ks + lane%4][8t + lane/4]
+// One thread issues cp.async.bulk (SASS UBLKCP) per stage with an mbarrier
+// transaction count; warps wait on the stage's full barrier and release it
+// through an empty barrier, so there is no CTA-wide __syncthreads in the loop
+// and fragment reads are conflict-free (lane-contiguous 8-byte loads).
+// ===========================================================================
+constexpr int kG3Stages = 3;
+constexpr int kG3KS = kGaussKC / 4;  // k-steps per chunk
 
-// Plan-time layouts (zero padded so the main loop needs no predicates):
-//   Dp  [gy*rows_cta][n_pad]  row blocks of rows_cta (gauss_row_blocks), n_pad = KC*ceil(n/KC)
-//   XT  [8*NT][n_pad]    X transposed, basis columns >= r are zero
-// Padding is exact: a padded l contributes exp(-0)*0 = 0, padded rows are not stored.
-__global__ void k_gauss_pack_xt(const double* __restrict__ X, int64_t n, int r, int64_t n_pad, int rows,
-                                double* __restrict__ XT) {
+__global__ void k_gauss_pack_dfrag(const double* __restrict__ D, int64_t ldd, int s, int64_t n, int gy,
+                                   int rows_cta, int64_t nchunks, double* __restrict__ Df) {
+  const int nrg = rows_cta / 8;
+  const int64_t tot = (int64_t)gy * nchunks * nrg * kG3KS * 32;
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (idx >= (int64_t)rows * n_pad) return;
-  int c = (int)(idx / n_pad);
-  int64_t l = idx - (int64_t)c * n_pad;
-  XT[idx] = (c < r && l < n) ? X[l * r + c] : 0.0;
+  if (idx >= tot) return;
+  int lane = (int)(idx & 31);
+  int64_t rest = idx >> 5;
+  int ks = (int)(rest % kG3KS); rest /= kG3KS;
+  int g = (int)(rest % nrg); rest /= nrg;
+  int64_t ch = rest % nchunks;
+  int rb = (int)(rest / nchunks);
+  int row = rb * rows_cta + 8 * g + (lane >> 2);
+  int64_t l = ch * kGaussKC + 4 * ks + (lane & 3);
+  Df[idx] = (row < s && l < n) ? D[(int64_t)row * ldd + l] : 0.0;
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+__global__ void k_gauss_pack_xfrag(const double* __restrict__ X, int64_t n, int r, int nt, int64_t nchunks,
+                                   double* __restrict__ Xf) {
+  const int64_t tot = nchunks * nt * kG3KS * 32;
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= tot) return;
+  int lane = (int)(idx & 31);
+  int64_t rest = idx >> 5;
+  int ks = (int)(rest % kG3KS); rest /= kG3KS;
+  int t = (int)(rest % nt);
+  int64_t ch = rest / nt;
+  int64_t l = ch * kGaussKC + 4 * ks + (lane & 3);
+  int c = 8 * t + (lane >> 2);
+  Xf[idx] = (c < r && l < n) ? X[l * r + c] : 0.0;
 }
 
-// grid = (ceil(P / PW), ceil(s_pad / (8*kGaussMaxWarps))); block = 32 * (row groups of this block)
-template <int NT, int PW, int MINB, bool SMEM_TAB>
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int NT>
+__host__ __device__ constexpr size_t gauss3_smem_bytes(int rows_cta) {
+  return (size_t)kG3Stages * (rows_cta / 8 + NT) * kG3KS * 32 * sizeof(double) + 2048 * sizeof(double) +
+         2 * kG3Stages * sizeof(uint64_t);
+}
+
+template <int NT, int PW, int MINB>
 __global__ void __launch_bounds__(32 * kGaussMaxWarps, MINB)
-k_gauss_rows(const double* __restrict__ Dp,     // s_pad x n_pad
-             const double* __restrict__ XT,     // 8NT x n_pad
-             const int64_t* __restrict__ S,     // s
-             const double* __restrict__ params, // P
-             int64_t P, int s, int64_t n_pad, int r, double ridge,
-             double* __restrict__ Mout) {       // P x s x r
-  constexpr int XR = 8 * NT;
-  extern __shared__ __align__(16) double gsm[];
+k_gauss_rows3(const double* __restrict__ Df, const double* __restrict__ Xf, const int64_t* __restrict__ S,
+              const double* __restrict__ params, int64_t P, int s, int64_t nchunks, int r, double ridge,
+              double* __restrict__ Mout) {
+  extern __shared__ __align__(128) double gsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nwarps = blockDim.x >> 5;
-  const int rows_cta = nwarps * 8;
-  const int row0 = blockIdx.y * rows_cta;  // first selected row of this CTA
-  const size_t stage_elems = (size_t)(rows_cta + XR) * kGaussLD;
+  const int nrg = blockDim.x >> 5;            // row groups = warps
+  const int rows_cta = nrg * 8;
+  const int row0 = blockIdx.y * rows_cta;
+  const int stage_d = (nrg + NT) * kG3KS * 32;  // doubles per stage
+  double* tab_s = gsm + (size_t)kG3Stages * stage_d;
+  uint64_t* full = reinterpret_cast<uint64_t*>(tab_s + 2048);
+  uint64_t* empty = full + kG3Stages;
+  const unsigned dbytes = (unsigned)(nrg * kG3KS * 32 * sizeof(double));
+  const unsigned xbytes = (unsigned)(NT * kG3KS * 32 * sizeof(double));
+  const double* dsrc = Df + (int64_t)blockIdx.y * nchunks * nrg * kG3KS * 32;
+
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < kG3Stages; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], nrg);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  for (int j = threadIdx.x; j < 2048; j += blockDim.x) tab_s[j] = g_exp2_tab2048[j];
+  __syncthreads();
+
+  auto issue = [&](int64_t ch) {
+    const int b = (int)(ch % kG3Stages);
+    if (ch >= kG3Stages) mbar_wait(&empty[b], (unsigned)(((ch / kG3Stages) - 1) & 1));
+    double* dst = gsm + (size_t)b * stage_d;
+    mbar_expect_tx(&full[b], dbytes + xbytes);
+    bulk_g2s(dst, dsrc + ch * (int64_t)nrg * kG3KS * 32, dbytes, &full[b]);
+    bulk_g2s(dst + nrg * kG3KS * 32, Xf + ch * (int64_t)NT * kG3KS * 32, xbytes, &full[b]);
+  };
+  if (threadIdx.x == 0)
+    for (int64_t c = 0; c < kG3Stages - 1 && c < nchunks; ++c) issue(c);
 
   const int64_t pbase = (int64_t)blockIdx.x * PW;
   double ninv[PW];
@@ -117,15 +189,9 @@ k_gauss_rows(const double* __restrict__ Dp,     // s_pad x n_pad
     const double sg = (p < P) ? params[p] : 1.0;
     ninv[u] = -(1.0 / (2.0 * sg * sg));  // reference: inv = 1.0 / (2.0 * sigma * sigma)
   }
-  const int lrow = warp * 8 + (lane >> 2);  // A-fragment row within the CTA
-  const int kq = lane & 3;                  // A-fragment column within the k-step
-  const int grow = row0 + lrow;
+  const int grow = row0 + warp * 8 + (lane >> 2);
   const int64_t srow = (grow < s) ? S[grow] : -1;
-  double* tab_s = gsm + (size_t)kGaussStages * stage_elems;
-  if (SMEM_TAB)
-    for (int j = threadIdx.x; j < 2048; j += blockDim.x) tab_s[j] = g_exp2_tab2048[j];
-  ExpTab tab{0.0, 0.0};
-  if (!SMEM_TAB) tab = exp_tab_load(lane);
+  const double onepr = 1.0 + ridge;  // the reference's exp(-0) + lam (_kernels.py:49)
 
   double acc[PW][NT][2];
 #pragma unroll
@@ -133,55 +199,31 @@ k_gauss_rows(const double* __restrict__ Dp,     // s_pad x n_pad
 #pragma unroll
     for (int t = 0; t < NT; ++t) acc[u][t][0] = acc[u][t][1] = 0.0;
 
-  const int64_t nchunks = n_pad / kGaussKC;
-  constexpr int kChunk16 = kGaussKC / 2;  // 16-byte pieces per row per stage
-  auto stage = [&](int64_t ch, int b) {
-    double* base = gsm + (size_t)b * stage_elems;
-    const int64_t l0 = ch * kGaussKC;
-    const int tot = (rows_cta + XR) * kChunk16;
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-      const int row = e / kChunk16, q = e - row * kChunk16;
-      const double* src = (row < rows_cta) ? Dp + (int64_t)(row0 + row) * n_pad + l0 + 2 * q
-                                           : XT + (int64_t)(row - rows_cta) * n_pad + l0 + 2 * q;
-      cp_async16(base + row * kGaussLD + 2 * q, src);
-    }
-  };
-
-#pragma unroll
-  for (int b = 0; b < kGaussStages - 1; ++b) {
-    if (b < nchunks) stage(b, b);
-    cp_async_commit();
-  }
   for (int64_t ch = 0; ch < nchunks; ++ch) {
-    cp_async_wait<kGaussStages - 2>();
-    __syncthreads();
-    {
-      const int64_t nx = ch + kGaussStages - 1;
-      if (nx < nchunks) stage(nx, (int)(nx % kGaussStages));
-      cp_async_commit();
-    }
-    const double* dsb = gsm + (size_t)(ch % kGaussStages) * stage_elems;
-    const double* xsb = dsb + (size_t)rows_cta * kGaussLD;
+    if (threadIdx.x == 0 && ch + kG3Stages - 1 < nchunks) issue(ch + kG3Stages - 1);
+    const int b = (int)(ch % kG3Stages);
+    mbar_wait(&full[b], (unsigned)((ch / kG3Stages) & 1));
+    const double* dsb = gsm + (size_t)b * stage_d + warp * kG3KS * 32 + lane;
+    const double* xsb = gsm + (size_t)b * stage_d + nrg * kG3KS * 32 + lane;
     const int64_t l0 = ch * kGaussKC;
     const int dcol = (srow >= l0 && srow < l0 + kGaussKC) ? (int)(srow - l0) : -1;
-#pragma unroll 1
-    for (int kk = 0; kk < kGaussKC; kk += 4) {
-      const double dv = dsb[lrow * kGaussLD + kk + kq];
+#pragma unroll 2
+    for (int ks = 0; ks < kG3KS; ++ks) {
+      const double dv = dsb[ks * 32];
       double bf[NT];
 #pragma unroll
-      for (int t = 0; t < NT; ++t) bf[t] = xsb[(t * 8 + (lane >> 2)) * kGaussLD + kk + kq];
-      const bool diag = (kk + kq) == dcol;
+      for (int t = 0; t < NT; ++t) bf[t] = xsb[(t * kG3KS + ks) * 32];
+      const bool diag = (4 * ks + (lane & 3)) == dcol;
 #pragma unroll
       for (int u = 0; u < PW; ++u) {
-        double e = SMEM_TAB ? sas_exp64_t2k(dv * ninv[u], tab_s) : sas_exp64(dv * ninv[u], tab);
-        if (diag) e = e + ridge;
+        const double e = sas_exp64_t2k_ridge(dv * ninv[u], tab_s, diag, onepr);
 #pragma unroll
         for (int t = 0; t < NT; ++t) dmma884(acc[u][t][0], acc[u][t][1], e, bf[t]);
       }
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[b]);
   }
-  cp_async_wait<0>();
-  // C fragment: lane holds C[lane/4][2*(lane%4) + {0,1}]
   if (grow < s) {
 #pragma unroll
     for (int u = 0; u < PW; ++u) {

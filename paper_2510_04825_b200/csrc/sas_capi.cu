@@ -112,8 +112,9 @@ struct sas_plan {
   int pdim = 0;
   double ridge = 0.0;
   double* D = nullptr;   // s_pad x n_pad squared distances (zero padded)
-  double* XT = nullptr;  // 8*ceil(r/8) x n_pad transposed basis (zero padded)
   int64_t n_pad = 0;
+  double* Dfrag = nullptr;  // K3 v3 fragment-ordered D
+  double* Xfrag = nullptr;  // K3 v3 fragment-ordered X^T
   // full operator for the residual checker
   int64_t* full_nbr = nullptr;
   double* full_phi = nullptr;
@@ -197,7 +198,7 @@ static void plan_free(sas_plan* pl) {
   if (!pl) return;
   DevGuard g(pl->device);
   void* ptrs[] = {pl->X, pl->S, pl->w, pl->t, pl->proj, pl->kind, pl->scale, pl->rate, pl->blocks,
-                  pl->phi, pl->G, pl->pts, pl->D, pl->XT, pl->full_nbr, pl->full_phi, pl->full_b,
+                  pl->phi, pl->G, pl->pts, pl->D, pl->Dfrag, pl->Xfrag, pl->full_nbr, pl->full_phi, pl->full_b,
                   pl->csr_rp_d, pl->csr_ci_d, pl->csr_va_d, pl->Mscr, pl->rpart, pl->fco,
                   pl->h_params, pl->h_ctab, pl->h_rhs, pl->h_coef, pl->h_sres, pl->h_outv,
                   pl->h_status, pl->h_bad};
@@ -365,13 +366,20 @@ extern "C" int sas_plan_create(const sas_desc* desc, const void* X, int64_t n, i
       const int xr = 8 * ((r + 7) / 8);
       pl->n_pad = ((n + kGaussKC - 1) / kGaussKC) * kGaussKC;
       TRY(dalloc(&pl->D, (size_t)s_pad * pl->n_pad * sizeof(double)));
-      TRY(dalloc(&pl->XT, (size_t)xr * pl->n_pad * sizeof(double)));
       cudaMemset(pl->D, 0, (size_t)s_pad * pl->n_pad * sizeof(double));
       int64_t tot = (int64_t)s * n;
       k_gauss_dist<<<(unsigned)((tot + 255) / 256), 256>>>(pl->pts, pl->S, n, pl->pdim, s, pl->n_pad, pl->D);
       int64_t totx = (int64_t)xr * pl->n_pad;
-      k_gauss_pack_xt<<<(unsigned)((totx + 255) / 256), 256>>>((const double*)pl->X, n, r, pl->n_pad, xr, pl->XT);
+      const int64_t nch = pl->n_pad / kGaussKC;
+      TRY(dalloc(&pl->Dfrag, (size_t)s_pad * pl->n_pad * sizeof(double)));
+      TRY(dalloc(&pl->Xfrag, (size_t)xr * pl->n_pad * sizeof(double)));
+      const int64_t totd = (int64_t)s_pad * pl->n_pad;
+      k_gauss_pack_dfrag<<<(unsigned)((totd + 255) / 256), 256>>>(pl->D, pl->n_pad, s, n, gy, rows_cta, nch, pl->Dfrag);
+      k_gauss_pack_xfrag<<<(unsigned)((totx + 255) / 256), 256>>>((const double*)pl->X, n, r, xr / 8, nch, pl->Xfrag);
+
       cudaError_t e = cudaDeviceSynchronize();
+      cudaFree(pl->D);  // only the fragment-ordered copy is used by the kernel
+      pl->D = nullptr;
       if (e != cudaSuccess) { plan_free(pl); sas_set_error("gauss plan: %s", cudaGetErrorString(e)); return SAS_ERR_CUDA; }
       break;
     }
@@ -486,19 +494,20 @@ static int launch_lsq(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t s
   return launch_lsq_t<T, 2, 16>(pl, a, as, scratch, st);
 }
 
-// K3 launch.  Variant (PW, min blocks/SM, exp table in smem) chosen per NT;
-// SAS_K3_VARIANT=<pw>,<minb>,<smemtab> overrides it for tuning runs.
-template <int NT, int PW, int MINB, bool TAB>
-static int launch_gauss_v(sas_plan* pl, const double* params, int64_t P, double* Mout, cudaStream_t st) {
+// K3 launch.  PW (parameter values per CTA) and min CTAs/SM per NT; for
+// NT == 3, SAS_K3_VARIANT=<pw>,<minb> overrides them in tuning runs.
+template <int NT, int PW, int MINB>
+static int launch_gauss3(sas_plan* pl, const double* params, int64_t P, double* Mout, cudaStream_t st) {
   int gy, rows_cta;
   gauss_row_blocks(pl->s, &gy, &rows_cta);
   const int nw = rows_cta / 8;
-  const size_t smem = gauss_smem_bytes<NT>(nw * 8);
-  auto kern = k_gauss_rows<NT, PW, MINB, TAB>;
+  const size_t smem = gauss3_smem_bytes<NT>(rows_cta);
+  auto kern = k_gauss_rows3<NT, PW, MINB>;
   SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((unsigned)((P + PW - 1) / PW), (unsigned)gy);
   stage_begin(pl, st, SAS_STAGE_GAUSS_ROWS);
-  kern<<<grid, 32 * nw, smem, st>>>(pl->D, pl->XT, pl->S, params, P, pl->s, pl->n_pad, pl->r, pl->ridge, Mout);
+  kern<<<grid, 32 * nw, smem, st>>>(pl->Dfrag, pl->Xfrag, pl->S, params, P, pl->s, pl->n_pad / kGaussKC, pl->r,
+                                    pl->ridge, Mout);
   stage_end(pl, st);
   SAS_CUDA_CHECK(cudaGetLastError());
   pl->last_launches++;
@@ -511,8 +520,8 @@ static int k3_variant() {
     const char* e = getenv("SAS_K3_VARIANT");
     v = 0;
     if (e) {
-      int pw = 0, mb = 0, tb = 0;
-      if (sscanf(e, "%d,%d,%d", &pw, &mb, &tb) == 3) v = pw * 100 + mb * 10 + tb;
+      int pw = 0, mb = 0;
+      if (sscanf(e, "%d,%d", &pw, &mb) == 2) v = pw * 10 + mb;
     }
   }
   return v;
@@ -522,16 +531,13 @@ template <int NT>
 static int launch_gauss_nt(sas_plan* pl, const double* params, int64_t P, double* Mout, cudaStream_t st) {
   if constexpr (NT == 3) {
     switch (k3_variant()) {
-      case 421: return launch_gauss_v<3, 4, 2, true>(pl, params, P, Mout, st);
-      case 420: return launch_gauss_v<3, 4, 2, false>(pl, params, P, Mout, st);
-      case 231: return launch_gauss_v<3, 2, 3, true>(pl, params, P, Mout, st);
-      case 230: return launch_gauss_v<3, 2, 3, false>(pl, params, P, Mout, st);
-      case 321: return launch_gauss_v<3, 3, 2, true>(pl, params, P, Mout, st);
-      case 221: return launch_gauss_v<3, 2, 2, true>(pl, params, P, Mout, st);
+      case 42: return launch_gauss3<3, 4, 2>(pl, params, P, Mout, st);
+      case 23: return launch_gauss3<3, 2, 3>(pl, params, P, Mout, st);
+      case 32: return launch_gauss3<3, 3, 2>(pl, params, P, Mout, st);
       default: break;
     }
   }
-  return launch_gauss_v<NT, gauss_pw<NT>(), 2, true>(pl, params, P, Mout, st);
+  return launch_gauss3<NT, gauss_pw<NT>(), 2>(pl, params, P, Mout, st);
 }
 
 static int launch_gauss(sas_plan* pl, const double* params, int64_t P, double* Mout, cudaStream_t st) {

@@ -254,6 +254,27 @@ __device__ __forceinline__ double sas_exp64_t2k(double x, const double* __restri
   return __hiloint2double(hi & keep, __double2loint(res) & keep);
 }
 
+// sas_exp64_t2k with the kernel-row ridge folded in: on the diagonal entry
+// (l == S_i) D = 0 exactly, so x = -0, r = +-0, q = +-0 and the result is the
+// table value; selecting (1 + ridge) instead of 2^0 gives exactly the
+// reference's exp(-0) + lam without an FP64 add.
+__device__ __forceinline__ double sas_exp64_t2k_ridge(double x, const double* __restrict__ tab_s, bool diag,
+                                                      double onepr) {
+  const double kd = fma(x, SAS_INVLN2X2K, SAS_EXP_MAGIC);
+  const int ki = __double2loint(kd);
+  const double kf = kd - SAS_EXP_MAGIC;
+  double r = fma(-kf, SAS_LN2D2K_HI, x);
+  r = fma(-kf, SAS_LN2D2K_LO, r);
+  double q = fma(r, 1.0 / 6.0, 0.5);
+  q = fma(q, r, 1.0);
+  q = q * r;
+  const double t = diag ? onepr : tab_s[ki & 2047];
+  const double res = fma(t, q, t);
+  const int hi = __double2hiint(res) + ((ki >> 11) << 20);
+  const int keep = (ki >= SAS_EXP2K_KMIN) ? -1 : 0;
+  return __hiloint2double(hi & keep, __double2loint(res) & keep);
+}
+
 // Host reference of the same algorithm (for the CPU accuracy test).
 double sas_exp64_host(double x);
 
