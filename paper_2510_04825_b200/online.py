@@ -45,8 +45,19 @@ _KIND_CODES = {"const": _capi.SAS_COEF_CONST, "linear": _capi.SAS_COEF_LINEAR,
                "exp": _capi.SAS_COEF_EXP}
 
 
-def _is_complex_value(v) -> bool:
-    return isinstance(v, complex) or np.iscomplexobj(v)
+def params_to_array(parameters, dp: int, pcomplex: bool) -> np.ndarray:
+    """Parameter list (floats, complex numbers or d_p-tuples, as the reference
+    accepts them, systems.py:61-65) -> the C-ABI layout: P x d_p doubles, or
+    P x d_p x 2 (re, im) for complex-parameter plans."""
+    vals = [np.atleast_1d(np.asarray(p, dtype=complex)).ravel() for p in parameters]
+    if any(v.size != dp for v in vals):
+        raise ValueError(f"parameters must have {dp} component(s)")
+    arr = np.array(vals, dtype=complex).reshape(len(vals), dp)
+    if pcomplex:
+        return np.ascontiguousarray(np.stack([arr.real, arr.imag], axis=-1))
+    if len(vals) and np.any(arr.imag != 0):
+        raise ValueError("complex parameter for a real-parameter plan")
+    return np.ascontiguousarray(arr.real)
 
 
 class GpuPlan:
@@ -158,15 +169,7 @@ class GpuPlan:
 
     # -- argument marshalling ------------------------------------------------
     def params_array(self, parameters) -> np.ndarray:
-        vals = [np.atleast_1d(np.asarray(p, dtype=complex)).ravel() for p in parameters]
-        if any(v.size != self.dp for v in vals):
-            raise ValueError(f"parameters must have {self.dp} component(s)")
-        arr = np.array(vals, dtype=complex).reshape(len(vals), self.dp)
-        if self.pcomplex:
-            return np.ascontiguousarray(np.stack([arr.real, arr.imag], axis=-1))
-        if len(vals) and np.any(arr.imag != 0):
-            raise ValueError("complex parameter for a real-parameter plan")
-        return np.ascontiguousarray(arr.real)
+        return params_to_array(parameters, self.dp, self.pcomplex)
 
     def coef_table(self, parameters) -> Optional[np.ndarray]:
         if not self.table_terms:
