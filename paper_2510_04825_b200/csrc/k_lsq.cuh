@@ -57,15 +57,29 @@ struct ParamView {
   }
 };
 
+// Cooperative group the assembler runs on: the whole CTA (k_lsq) or one warp
+// (k_lsq_warp, one parameter value per warp).
+struct CtaGroup {
+  __device__ __forceinline__ int rank() const { return threadIdx.x; }
+  __device__ __forceinline__ int size() const { return blockDim.x; }
+  __device__ __forceinline__ void sync() const { __syncthreads(); }
+};
+struct WarpGroup {
+  __device__ __forceinline__ int rank() const { return threadIdx.x & 31; }
+  __device__ __forceinline__ int size() const { return 32; }
+  __device__ __forceinline__ void sync() const { __syncwarp(); }
+};
+
 // ---------------------------------------------------------------------------
 template <typename T>
 struct AsmGlobal {
   const T* M;  // P x s x r
   static constexpr size_t scratch_bytes(int, int) { return 0; }
-  __device__ __forceinline__ void operator()(int64_t p, T* Ms, int ldm, int s, int r,
+  template <class Grp>
+  __device__ __forceinline__ void operator()(const Grp& g, int64_t p, T* Ms, int ldm, int s, int r,
                                              unsigned char*) const {
     const T* src = M + p * (int64_t)s * r;
-    for (int idx = threadIdx.x; idx < s * r; idx += blockDim.x) {
+    for (int idx = g.rank(); idx < s * r; idx += g.size()) {
       int i = idx / r, j = idx - i * r;
       Ms[i * ldm + j] = src[idx];
     }
@@ -119,19 +133,20 @@ struct AsmAffine {
   ParamView pv;
   const double* coef_table;   // P x K x 2 or nullptr
   static constexpr size_t scratch_bytes(int, int) { return 16 * sizeof(T); }
-  __device__ __forceinline__ void operator()(int64_t p, T* Ms, int ldm, int s, int r,
+  template <class Grp>
+  __device__ __forceinline__ void operator()(const Grp& g, int64_t p, T* Ms, int ldm, int s, int r,
                                              unsigned char* scratch) const {
     T* f = reinterpret_cast<T*>(scratch);
-    if (threadIdx.x < K) {
-      int k = threadIdx.x;
+    if (g.rank() < K) {
+      int k = g.rank();
       cplx sc{scale[2 * k], scale[2 * k + 1]};
       cplx rt = rate ? cplx{rate[2 * k], rate[2 * k + 1]} : cplx{0.0, 0.0};
       const double* tab = coef_table ? coef_table + (p * K + k) * 2 : nullptr;
       f[k] = AffineCoef<T>::eval(kind[k], sc, rt, pv.get(p, 0), tab);
     }
-    __syncthreads();
+    g.sync();
     const int64_t blk = (int64_t)s * r;
-    for (int idx = threadIdx.x; idx < s * r; idx += blockDim.x) {
+    for (int idx = g.rank(); idx < s * r; idx += g.size()) {
       int i = idx / r, j = idx - i * r;
       // m = f0*B0; m = m + fk*Bk  (online.py:110-112, numpy elementwise order)
       T m = Sc<T>::mul_exact(f[0], blocks[idx]);
@@ -152,26 +167,27 @@ struct AsmStencil {
   double hh;
   const double* params;  // P x dp (real)
   static size_t scratch_bytes(int s, int E) { return (size_t)s * (E + 1) * sizeof(double); }
-  __device__ __forceinline__ void operator()(int64_t p, double* Ms, int ldm, int s, int r,
+  template <class Grp>
+  __device__ __forceinline__ void operator()(const Grp& g, int64_t p, double* Ms, int ldm, int s, int r,
                                              unsigned char* scratch) const {
     double* cs = reinterpret_cast<double*>(scratch);
     const double* pp = params + p * dp;
     const int E1 = E + 1;
-    for (int idx = threadIdx.x; idx < s * E; idx += blockDim.x) {
+    for (int idx = g.rank(); idx < s * E; idx += g.size()) {
       int i = idx / E, e = idx - i * E;
       const double* ph = phi + (int64_t)idx * dp;
       double arg = dmul_exact(pp[0], ph[0]);
       for (int k = 1; k < dp; ++k) arg = dadd_exact(arg, dmul_exact(pp[k], ph[k]));
       cs[i * E1 + 1 + e] = exp(arg) / hh;
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < s; i += blockDim.x) {
+    g.sync();
+    for (int i = g.rank(); i < s; i += g.size()) {
       double d = 0.0;
       for (int e = 0; e < E; ++e) d = dadd_exact(d, cs[i * E1 + 1 + e]);
       cs[i * E1] = d;
     }
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < s * r; idx += blockDim.x) {
+    g.sync();
+    for (int idx = g.rank(); idx < s * r; idx += g.size()) {
       int i = idx / r, j = idx - i * r;
       const double* g = G + (int64_t)i * E1 * r + j;
       double m = cs[i * E1] * g[0];
@@ -213,7 +229,7 @@ __global__ void __launch_bounds__(512) k_lsq(LsqArgs<T> a, Asm as, size_t scratc
   (void)scratch_bytes;
 
   for (int64_t p = blockIdx.x; p < a.P; p += gridDim.x) {
-    as(p, Ms, ldm, s, r, scratch);
+    as(CtaGroup{}, p, Ms, ldm, s, r, scratch);
     for (int i = threadIdx.x; i < s; i += nthr) Ms[i * ldm + r] = a.t[p * a.t_stride + i];
     __syncthreads();
 

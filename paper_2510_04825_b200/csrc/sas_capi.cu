@@ -16,6 +16,7 @@
 #include "../../include/sas.h"
 #include "sas_common.cuh"
 #include "k_lsq.cuh"
+#include "k_lsq_warp.cuh"
 #include "k_gauss.cuh"
 #include "k_recon.cuh"
 
@@ -460,9 +461,8 @@ static int launch_lsq_t(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t
   const int W = (a.s + RPT - 1) / RPT;
   const size_t smem = lsq_smem_bytes<T>(a.s, a.r, W, NC, scratch);
   auto kern = k_lsq<T, NC, RPT, Asm>;
-  static int configured_dev_mask = 0;
-  (void)configured_dev_mask;
   SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   int occ = 0;
   SAS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * W, smem));
   if (occ < 1) {
@@ -480,9 +480,64 @@ static int launch_lsq_t(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t
   return SAS_OK;
 }
 
+template <typename T, int RA, int CB, class Asm>
+static int launch_lsq_warp_t(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t scratch, cudaStream_t st) {
+  constexpr int kWarps = 2;  // parameter values per CTA (one per warp)
+  const size_t smem = kWarps * lsq_warp_smem_per_warp<T>(a.s, a.r, scratch);
+  auto kern = k_lsq_warp<T, RA, CB, Asm>;
+  SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  int occ = 0;
+  SAS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * kWarps, smem));
+  if (occ < 1) {
+    sas_set_error("least-squares warp kernel does not fit (s=%d r=%d smem=%zu)", a.s, a.r, smem);
+    return SAS_ERR_ARG;
+  }
+  int64_t grid = (int64_t)occ * pl->sms;
+  const int64_t need = (a.P + kWarps - 1) / kWarps;
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  stage_begin(pl, st, SAS_STAGE_LSQ);
+  kern<<<(unsigned)grid, 32 * kWarps, smem, st>>>(a, as, scratch);
+  stage_end(pl, st);
+  SAS_CUDA_CHECK(cudaGetLastError());
+  pl->last_launches++;
+  return SAS_OK;
+}
+
+static bool lsq_force_cta() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SAS_LSQ_KERNEL");
+    v = (e && strcmp(e, "cta") == 0) ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// Warp-per-parameter kernel when [M_w | t_w] fits a warp's registers, else
+// the CTA-per-parameter kernel.
 template <typename T, class Asm>
 static int launch_lsq(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t scratch, cudaStream_t st) {
-  const bool two = (a.r + 1) > 32;
+  const int cols = a.r + 1;
+  if (!lsq_force_cta()) {
+    if constexpr (std::is_same<T, double>::value) {
+      if (cols <= 12) {
+        if (a.s <= 24) return launch_lsq_warp_t<T, 3, 3>(pl, a, as, scratch, st);
+        if (a.s <= 40) return launch_lsq_warp_t<T, 5, 3>(pl, a, as, scratch, st);
+        if (a.s <= 80) return launch_lsq_warp_t<T, 10, 3>(pl, a, as, scratch, st);
+        if (a.s <= 128) return launch_lsq_warp_t<T, 16, 3>(pl, a, as, scratch, st);
+      } else if (cols <= 24) {
+        if (a.s <= 40) return launch_lsq_warp_t<T, 5, 6>(pl, a, as, scratch, st);
+        if (a.s <= 80) return launch_lsq_warp_t<T, 10, 6>(pl, a, as, scratch, st);
+      } else if (cols <= 32) {
+        if (a.s <= 40) return launch_lsq_warp_t<T, 5, 8>(pl, a, as, scratch, st);
+      }
+    } else {
+      if (cols <= 12 && a.s <= 24) return launch_lsq_warp_t<T, 3, 3>(pl, a, as, scratch, st);
+      if (cols <= 12 && a.s <= 40) return launch_lsq_warp_t<T, 5, 3>(pl, a, as, scratch, st);
+    }
+  }
+  const bool two = cols > 32;
   if (!two) {
     if (a.s <= 64) return launch_lsq_t<T, 1, 4>(pl, a, as, scratch, st);
     if (a.s <= 128) return launch_lsq_t<T, 1, 8>(pl, a, as, scratch, st);
