@@ -1,0 +1,150 @@
+"""Throughput and full-size parity spot checks for all five BASELINE configs on one GPU.
+
+    python tools/bench_configs.py [--configs 1,2,3,4,5] [--steps 5] [--out gpurun_out/configs.jsonl]
+
+For each config: build the problem at its BASELINE size, obtain X and S
+(offline: host sparse solves for config 1, GPU Cholesky for config 2, GPU CG
+for config 3; configs 4 and 5 use a seeded orthonormal synthetic basis because
+their snapshot solves are impractical here -- the online cost does not depend
+on the values of X), then time the device-resident online sweep of the
+config's per-GPU parameter count and compare a few parameters against the CPU
+oracle at full size.  One JSON line per config.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import torch  # noqa: E402
+
+from oracle import online_ref  # noqa: E402
+from paper_2510_04825_b200 import _capi, online, problems  # noqa: E402
+from paper_2510_04825_b200.offline import (RowSelector, SnapshotBasis, anchor_product, choose_anchor,  # noqa: E402
+                                           offline, select_rows)
+from paper_2510_04825_b200.systems import GaussianKernelOperator, StencilOperator  # noqa: E402
+
+P_PER_GPU = {1: 1000, 2: 4096, 3: 65_536, 4: 100_000, 5: 125_000}
+
+
+def synthetic_basis(prob, r, complex_=False, seed=7, device=None):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    n = prob.system.n
+    a = torch.randn(n, r, generator=g, dtype=torch.float64)
+    if complex_:
+        a = torch.complex(a, torch.randn(n, r, generator=g, dtype=torch.float64))
+    if device is not None:
+        a = a.to(device)
+    q, _ = torch.linalg.qr(a)
+    X = q.cpu().numpy()
+    basis = SnapshotBasis(points=tuple(prob.snapshot_points[:r]), raw=X, basis=X, singular_values=np.ones(r))
+    anchor = choose_anchor(prob.snapshot_points)
+    b_anchor = anchor_product(prob.system, anchor, X)
+    sel = select_rows(b_anchor, prob.system.full_rhs(anchor), strategy="leverage",
+                      oversample=prob.samples / (r + 1), seed=prob.selector_seed)
+    return basis, sel
+
+
+def oracle_coef(prob, basis, sel, p):
+    sysm = prob.system
+    X, idx = basis.basis, sel.indices
+    if sysm.affine_terms is not None:
+        blocks = online_ref.affine_blocks([t.matrix for t in sysm.affine_terms], X, idx)
+        coeffs = [complex(t.scale) if t.kind == "const" else complex(t.scale) * p for t in sysm.affine_terms]
+        m = online_ref.affine_combine(coeffs, blocks)
+    elif isinstance(sysm.operator, GaussianKernelOperator):
+        op = sysm.operator
+        m = online_ref.sampled_rows(lambda q, rows: online_ref.gauss_rows(op.points, rows, float(q), op.ridge),
+                                    X, idx, p)
+    else:
+        op = sysm.operator
+        m = online_ref.sampled_rows(lambda q, rows: online_ref.stencil_rows(op, q, rows), X, idx, p)
+    t = sysm.rhs(p, idx)
+    c, sres, _ = online_ref.solve_one(m, t, sel.weights)
+    floor = online_ref.ls_floor(m, t, sel.weights, draws=2)
+    return c, sres, floor
+
+
+def run(cfg, steps, dev):
+    t0 = time.perf_counter()
+    prob = problems.build(cfg)
+    if cfg in (1, 2):
+        basis, sel = offline(prob, device=dev)
+        src = "offline (reference recipe)"
+    elif cfg == 3:
+        basis, sel = offline(prob, device=dev, prefer_cg=True)
+        src = "offline (GPU CG snapshots)"
+    elif cfg == 4:
+        basis, sel = synthetic_basis(prob, 8, complex_=True, device=dev)
+        src = "synthetic orthonormal basis r'=8 (complex)"
+    else:
+        basis, sel = synthetic_basis(prob, 50, device=dev)
+        src = "synthetic orthonormal basis r=50"
+    t_off = time.perf_counter() - t0
+    plan = online.precompute_online(prob.system, basis, sel, device=0)
+    P = P_PER_GPU[cfg]
+    params = prob.test_params(P)
+    pt = online.device_params(plan, params, device=dev)
+    out = online.alloc_outputs(plan, P, device=dev)
+    online.solve_device(plan, pt, out)
+    torch.cuda.synchronize()
+    g = plan.gpu
+    g.set_timing(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stage = {}
+    total = 0.0
+    for _ in range(steps):
+        ev0.record()
+        online.solve_device(plan, pt, out)
+        ev1.record()
+        torch.cuda.synchronize()
+        total += ev0.elapsed_time(ev1)
+        for sid, ms in g.stage_times():
+            stage.setdefault(sid, []).append(ms)
+    g.set_timing(False)
+    ms = total / steps
+    st = out["status"].cpu().numpy()
+    coef = out["coef"].cpu().numpy()
+    # full-size parity spot check against the oracle
+    worst = 0.0
+    checks = []
+    for k in np.linspace(0, P - 1, 4).astype(int):
+        c, sres, floor = oracle_coef(prob, basis, sel, params[k])
+        d = float(np.linalg.norm(coef[k] - c) / np.linalg.norm(c))
+        checks.append({"k": int(k), "rel_diff": d, "floor": float(floor)})
+        worst = max(worst, d / max(1e-10, 10 * floor))
+    return {
+        "config": cfg, "name": prob.key, "n": prob.system.n, "r": basis.rank, "s": sel.size, "P": P,
+        "dtype": "c128" if g.complex else "f64", "basis": src, "offline_s": round(t_off, 1),
+        "ms_per_sweep": round(ms, 3), "p_per_s": round(P / ms * 1e3, 1),
+        "stage_ms": {("K3" if k == _capi.SAS_STAGE_GAUSS_ROWS else "K4"): round(sum(v) / steps, 3)
+                     for k, v in stage.items()},
+        "status_ok": bool(np.all(st == 0)), "parity": checks, "parity_ok": bool(worst <= 1.0),
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="1,2,3,4,5")
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    dev = torch.device("cuda:0")
+    for cfg in [int(c) for c in args.configs.split(",")]:
+        res = run(cfg, args.steps, dev)
+        line = json.dumps(res)
+        print(line, flush=True)
+        if args.out:
+            with open(args.out, "a") as fh:
+                fh.write(line + "\n")
+
+
+if __name__ == "__main__":
+    main()
