@@ -17,6 +17,7 @@
 #include "sas_common.cuh"
 #include "k_lsq.cuh"
 #include "k_lsq_warp.cuh"
+#include "k_lsq_mw.cuh"
 #include "k_gauss.cuh"
 #include "k_recon.cuh"
 
@@ -505,6 +506,43 @@ static int launch_lsq_warp_t(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, s
   return SAS_OK;
 }
 
+template <typename T, int RG, int RA, int CB, class Asm>
+static int launch_lsq_mw_t(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t scratch, cudaStream_t st) {
+  const int W = (a.s + RG * RA - 1) / (RG * RA);
+  if (W > 8) {
+    sas_set_error("least-squares multi-warp kernel: s=%d too large for RA=%d", a.s, RA);
+    return SAS_ERR_ARG;
+  }
+  const size_t smem = lsq_mw_smem_bytes<T>(a.s, a.r, W, scratch);
+  auto kern = k_lsq_mw<T, RG, RA, CB, Asm>;
+  SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  int occ = 0;
+  SAS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * W, smem));
+  if (occ < 1) {
+    sas_set_error("least-squares multi-warp kernel does not fit (s=%d r=%d smem=%zu)", a.s, a.r, smem);
+    return SAS_ERR_ARG;
+  }
+  int64_t grid = (int64_t)occ * pl->sms;
+  if (grid > a.P) grid = a.P;
+  if (grid < 1) grid = 1;
+  stage_begin(pl, st, SAS_STAGE_LSQ);
+  kern<<<(unsigned)grid, 32 * W, smem, st>>>(a, as, scratch);
+  stage_end(pl, st);
+  SAS_CUDA_CHECK(cudaGetLastError());
+  pl->last_launches++;
+  return SAS_OK;
+}
+
+static int lsq_ra_pref() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SAS_LSQ_RA");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 static bool lsq_force_cta() {
   static int v = -1;
   if (v < 0) {
@@ -514,13 +552,19 @@ static bool lsq_force_cta() {
   return v == 1;
 }
 
-// Warp-per-parameter kernel when [M_w | t_w] fits a warp's registers, else
-// the CTA-per-parameter kernel.
+// Kernel choice for the batched least squares (all three compute the same
+// Householder LS, they differ in how many warps share one parameter value):
+//   k_lsq_warp  one warp per p, [M_w | t_w] in one warp's registers (small s, r)
+//   k_lsq_mw    W <= 8 warps per p, registers + one CTA barrier per column step
+//   k_lsq       CTA per p fallback (s up to 512)
+// SAS_LSQ_KERNEL=cta forces the fallback; SAS_LSQ_RA=4 picks the 4-row variant
+// of k_lsq_mw (tuning).
 template <typename T, class Asm>
 static int launch_lsq(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t scratch, cudaStream_t st) {
   const int cols = a.r + 1;
+  constexpr bool real = std::is_same<T, double>::value;
   if (!lsq_force_cta()) {
-    if constexpr (std::is_same<T, double>::value) {
+    if (real) {
       if (cols <= 12) {
         if (a.s <= 24) return launch_lsq_warp_t<T, 3, 3>(pl, a, as, scratch, st);
         if (a.s <= 40) return launch_lsq_warp_t<T, 5, 3>(pl, a, as, scratch, st);
@@ -536,15 +580,33 @@ static int launch_lsq(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t s
       if (cols <= 12 && a.s <= 24) return launch_lsq_warp_t<T, 3, 3>(pl, a, as, scratch, st);
       if (cols <= 12 && a.s <= 40) return launch_lsq_warp_t<T, 5, 3>(pl, a, as, scratch, st);
     }
+    const bool ra4 = lsq_ra_pref() == 4;
+    if (real) {
+      // RG = 4 row groups x 8 column groups per warp
+      if (ra4 && a.s <= 128) {
+        if (cols <= 32) return launch_lsq_mw_t<T, 4, 4, 4>(pl, a, as, scratch, st);
+        if (cols <= 48) return launch_lsq_mw_t<T, 4, 4, 6>(pl, a, as, scratch, st);
+        return launch_lsq_mw_t<T, 4, 4, 8>(pl, a, as, scratch, st);
+      }
+      if (a.s <= 256) {
+        if (cols <= 32) return launch_lsq_mw_t<T, 4, 8, 4>(pl, a, as, scratch, st);
+        if (cols <= 48) return launch_lsq_mw_t<T, 4, 8, 6>(pl, a, as, scratch, st);
+        return launch_lsq_mw_t<T, 4, 8, 8>(pl, a, as, scratch, st);
+      }
+    } else {
+      // complex: RG = 8 x 4 column groups for narrow bases, 4 x 8 otherwise
+      if (cols <= 12) {
+        if (ra4 && a.s <= 256) return launch_lsq_mw_t<T, 8, 4, 3>(pl, a, as, scratch, st);
+        if (a.s <= 512) return launch_lsq_mw_t<T, 8, 8, 3>(pl, a, as, scratch, st);
+      } else if (cols <= 32 && a.s <= 256) {
+        return launch_lsq_mw_t<T, 4, 8, 4>(pl, a, as, scratch, st);
+      }
+    }
   }
-  const bool two = cols > 32;
-  if (!two) {
-    if (a.s <= 64) return launch_lsq_t<T, 1, 4>(pl, a, as, scratch, st);
+  if (cols <= 32) {
     if (a.s <= 128) return launch_lsq_t<T, 1, 8>(pl, a, as, scratch, st);
-    if (a.s <= 256) return launch_lsq_t<T, 1, 16>(pl, a, as, scratch, st);
     return launch_lsq_t<T, 1, 32>(pl, a, as, scratch, st);
   }
-  if (a.s <= 64) return launch_lsq_t<T, 2, 4>(pl, a, as, scratch, st);
   if (a.s <= 128) return launch_lsq_t<T, 2, 8>(pl, a, as, scratch, st);
   return launch_lsq_t<T, 2, 16>(pl, a, as, scratch, st);
 }

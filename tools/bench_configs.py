@@ -72,10 +72,14 @@ def oracle_coef(prob, basis, sel, p):
     return c, sres, floor
 
 
-def run(cfg, steps, dev):
+def run(cfg, steps, dev, synthetic=False, P=None, check=True):
     t0 = time.perf_counter()
     prob = problems.build(cfg)
-    if cfg in (1, 2):
+    if synthetic and cfg != 2:
+        r = {1: 8, 3: 40, 4: 8, 5: 50}[cfg]
+        basis, sel = synthetic_basis(prob, r, complex_=(cfg == 4), device=dev)
+        src = f"synthetic orthonormal basis r={r}"
+    elif cfg in (1, 2):
         basis, sel = offline(prob, device=dev)
         src = "offline (reference recipe)"
     elif cfg == 3:
@@ -89,7 +93,7 @@ def run(cfg, steps, dev):
         src = "synthetic orthonormal basis r=50"
     t_off = time.perf_counter() - t0
     plan = online.precompute_online(prob.system, basis, sel, device=0)
-    P = P_PER_GPU[cfg]
+    P = P or P_PER_GPU[cfg]
     params = prob.test_params(P)
     pt = online.device_params(plan, params, device=dev)
     out = online.alloc_outputs(plan, P, device=dev)
@@ -115,7 +119,7 @@ def run(cfg, steps, dev):
     # full-size parity spot check against the oracle
     worst = 0.0
     checks = []
-    for k in np.linspace(0, P - 1, 4).astype(int):
+    for k in (np.linspace(0, P - 1, 4).astype(int) if check else []):
         c, sres, floor = oracle_coef(prob, basis, sel, params[k])
         d = float(np.linalg.norm(coef[k] - c) / np.linalg.norm(c))
         checks.append({"k": int(k), "rel_diff": d, "floor": float(floor)})
@@ -135,10 +139,13 @@ def main():
     ap.add_argument("--configs", default="1,2,3,4,5")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--synthetic", action="store_true", help="seeded orthonormal basis for every config but 2")
+    ap.add_argument("--P", type=int, default=None)
+    ap.add_argument("--no-parity", action="store_true")
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     for cfg in [int(c) for c in args.configs.split(",")]:
-        res = run(cfg, args.steps, dev)
+        res = run(cfg, args.steps, dev, synthetic=args.synthetic, P=args.P, check=not args.no_parity)
         line = json.dumps(res)
         print(line, flush=True)
         if args.out:
