@@ -1,30 +1,183 @@
-// K4m: batched weighted least squares, W warps cooperating on one parameter
-// value, for matrices too large for one warp's registers (configs 3, 4, 5:
-// 160x41, 120x9 complex, 200x51).  Same contract as k_lsq / k_lsq_warp
-// (linalg.solve_ls, linalg.py:89-113, called from online.py:105-134).
+// K4: batched weighted least squares, W <= 8 warps cooperating on one
+// parameter value (W = 1 for small problems).  Replaces linalg.solve_ls
+// (reference linalg.py:89-113) as called from online.solve_online
+// (online.py:105-134):
 //
-// Layout: lane = a + RG*b (a < RG row groups, b < CG = 32/RG column groups).
-// Global row group of a lane = w*RG + a (w = warp), so row i belongs to
-// (row group i mod (W*RG), slot u = i / (W*RG)); column j to (b = j mod CG,
-// slot v = j / CG).  Registers A[RA][CB].
+//   M_w = diag(w) M, t_w = diag(w) t           (linalg.py:102-105)
+//   Householder QR of [M_w | t_w]              (np.linalg.qr, linalg.py:106)
+//   rank test  min|R_ii| < 1e-12 max|R_ii|      (linalg.py:107-112)
+//   c = R^{-1} (Q^H t_w)[:r]                    (solve_triangular, linalg.py:113)
+//   sampled residual ||w * (M c - t)||          (online.py:121-124, recomputed
+//                                                explicitly from the unweighted M)
+//   output value  (c^H X) c                     (online.py:125-127)
 //
-// Householder step k (Gram-row formulation):
-//   x_i = M_ik for own rows           <- shuffle inside the warp (column group k mod CG)
-//   partial g_j over own rows, butterfly over the RG row groups of the warp
-//   warp partials and row k go to shared memory (double-buffered), ONE
-//   __syncthreads, every thread sums the W partials of its columns in warp
-//   order (deterministic), forms beta/tau and updates its rows.
+// Layout: lane = a + RG*b (a < RG row groups, b < CG = 32/RG column groups);
+// the global row group of a lane is w*RG + a, so row i lives in row group
+// i mod (W*RG), slot u = i / (W*RG); column j (the rhs is column r) in column
+// group j mod CG, slot v = j / CG.  The augmented matrix sits in registers
+// A[RA][CB]; the unweighted M(p) stays in shared memory for the residual.
+//
+// Householder step k, Gram-row formulation (one reduction per column):
+//   x_i = M_ik            shuffle from column group k mod CG of the same rows
+//   g_j = sum_i conj(x_i) M_ij    own rows, butterfly over the warp's RG row
+//                         groups, warp partials in shared memory, ONE barrier,
+//                         every thread sums the W partials in warp order
+//   |x| = sqrt(g_kk), beta = -e^{i arg M_kk} |x|, tau = 2 / v^H v
+//   M_ij -= tau v_i (g_j - conj(beta) M_kj)      for j > k
+// The column loop is split as k = bk + CG*vk with the slot vk unrolled, so the
+// register slot of column k is a compile-time index and finished column slots
+// (v < vk) drop out of the unrolled code.  Reductions are in a fixed order:
+// results do not depend on the grid, the batch or the number of GPUs.
+//
+// The assembler functor fills shared memory with the unweighted M(p):
+//   AsmGlobal  - M precomputed by another kernel (Gaussian kernel rows, K3)
+//   AsmAffine  - M = sum_k f_k(p) B_k with numpy's operation order (K1)
+//   AsmStencil - edge-form stencil rows with exp-affine coefficients (K2)
 #pragma once
-#include "k_lsq_warp.cuh"
+#include "k_lsq.cuh"
+
+template <typename T>
+__device__ __forceinline__ T shfl_t(T v, int src);
+template <>
+__device__ __forceinline__ double shfl_t<double>(double v, int src) {
+  return __shfl_sync(0xffffffffu, v, src);
+}
+template <>
+__device__ __forceinline__ cplx shfl_t<cplx>(cplx v, int src) {
+  return cplx{__shfl_sync(0xffffffffu, v.re, src), __shfl_sync(0xffffffffu, v.im, src)};
+}
+template <typename T>
+__device__ __forceinline__ T shfl_xor_t(T v, int m);
+template <>
+__device__ __forceinline__ double shfl_xor_t<double>(double v, int m) {
+  return __shfl_xor_sync(0xffffffffu, v, m);
+}
+template <>
+__device__ __forceinline__ cplx shfl_xor_t<cplx>(cplx v, int m) {
+  return cplx{__shfl_xor_sync(0xffffffffu, v.re, m), __shfl_xor_sync(0xffffffffu, v.im, m)};
+}
+
+// 1/x to ~1 ulp: hardware reciprocal seed (MUFU.RCP64H) + two Newton steps.
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
 
 template <typename T>
 __host__ __device__ inline size_t lsq_mw_smem_bytes(int s, int r, int W, size_t scratch) {
   const int ldm = r + 1;
-  // Ms (s x ldm), R/y (r x ldm), c (r), 2 x [row k (ldm) + partials (W x ldm)]
-  size_t n = (size_t)s * ldm + (size_t)r * ldm + r + 2 * ((size_t)ldm + (size_t)W * ldm);
+  // Ms (s x ldm), R/y (r x ldm), c (r), R_kk (r), 2 x [row k (ldm) + partials (W x ldm)]
+  size_t n = (size_t)s * ldm + (size_t)r * ldm + 2 * (size_t)r + 2 * ((size_t)ldm + (size_t)W * ldm);
   size_t bytes = (n * sizeof(T) + 15) / 16 * 16;
-  return bytes + 128 + (scratch + 15) / 16 * 16;
+  return bytes + 16 * sizeof(double) + (scratch + 15) / 16 * 16;
 }
+
+template <typename T, int RG, int RA, int CB>
+struct LsqStep {
+  using S = Sc<T>;
+  static constexpr int CG = 32 / RG;
+  // One Householder step for column k = bk + CG*VK (VK compile-time).
+  template <int VK>
+  static __device__ __forceinline__ void run(T (&A)[RA][CB], int k, int bk, int gk, int uk, int la, int lb,
+                                             int grg, int nrg, int W, int warp, int r, int ldm, T* rk_s,
+                                             T* pt, T* rdiag, double& dmax, double& dmin, int& amin) {
+    // x_i = M_ik for own rows; rows above k contribute nothing
+    T xg[RA];
+#pragma unroll
+    for (int u = 0; u < RA; ++u) {
+      const T xv = shfl_t(A[u][VK], la + RG * bk);
+      xg[u] = (grg + nrg * u >= k) ? xv : S::zero();
+    }
+    // owner of row k publishes it
+    if (grg == gk) {
+#pragma unroll
+      for (int u = 0; u < RA; ++u)
+        if (u == uk) {
+#pragma unroll
+          for (int v = VK; v < CB; ++v) {
+            const int j = lb + CG * v;
+            if (j >= k && j <= r) rk_s[j] = A[u][v];
+          }
+        }
+    }
+    // Gram row over own rows, butterfly over the RG row groups of the warp
+#pragma unroll
+    for (int v = VK; v < CB; ++v) {
+      T acc = S::zero();
+#pragma unroll
+      for (int u = 0; u < RA; ++u) acc = S::fma_conj(xg[u], A[u][v], acc);
+#pragma unroll
+      for (int off = 1; off < RG; off <<= 1) acc = S::add(acc, shfl_xor_t(acc, off));
+      const int j = lb + CG * v;
+      if (la == 0 && j >= k && j <= r) pt[warp * ldm + j] = acc;
+    }
+    __syncthreads();
+    double gkk = 0.0;
+    for (int w = 0; w < W; ++w) gkk += S::re(pt[w * ldm + k]);
+    const T alpha = rk_s[k];
+    const double nrm = sqrt(gkk);
+    const double aa = S::abs(alpha);
+    T beta;
+    double tau;
+    if (nrm == 0.0) {
+      beta = S::zero();
+      tau = 0.0;
+    } else {
+      beta = (aa == 0.0) ? S::from(-nrm, 0.0) : S::mulr(alpha, -nrm * rcp_nr(aa));
+      tau = rcp_nr(nrm * (nrm + aa));  // 2 / (v^H v)
+    }
+    if (threadIdx.x == 0) rdiag[k] = beta;
+    dmax = fmax(dmax, nrm);
+    if (nrm < dmin) { dmin = nrm; amin = k; }
+    T sj[CB];
+#pragma unroll
+    for (int v = VK; v < CB; ++v) {
+      const int j = lb + CG * v;
+      sj[v] = S::zero();
+      if (j > k && j <= r) {
+        T g = S::zero();
+        for (int w = 0; w < W; ++w) g = S::add(g, pt[w * ldm + j]);
+        sj[v] = S::mulr(S::sub(g, S::mul(S::conj(beta), rk_s[j])), tau);
+      }
+    }
+    // v_i: x_i below the diagonal, alpha - beta on it, 0 above
+    const T vdiag = S::sub(alpha, beta);
+#pragma unroll
+    for (int u = 0; u < RA; ++u) {
+      const int i = grg + nrg * u;
+      const T vi = (i == k) ? vdiag : xg[u];
+#pragma unroll
+      for (int v = VK; v < CB; ++v) A[u][v] = S::fms(vi, sj[v], A[u][v]);
+    }
+  }
+};
+
+template <typename T, int RG, int RA, int CB, int VK>
+struct LsqColumns {
+  static __device__ __forceinline__ void run(T (&A)[RA][CB], int& gk, int& uk, int la, int lb, int grg, int nrg,
+                                             int W, int warp, int r, int ldm, T* rowb, T* part, T* rdiag,
+                                             double& dmax, double& dmin, int& amin) {
+    constexpr int CG = 32 / RG;
+    if (VK * CG >= r) return;
+#pragma unroll 1
+    for (int bk = 0; bk < CG; ++bk) {
+      const int k = bk + CG * VK;
+      if (k >= r) break;
+      const int buf = k & 1;
+      LsqStep<T, RG, RA, CB>::template run<VK>(A, k, bk, gk, uk, la, lb, grg, nrg, W, warp, r, ldm,
+                                               rowb + buf * ldm, part + (size_t)buf * W * ldm, rdiag, dmax,
+                                               dmin, amin);
+      if (++gk == nrg) { gk = 0; ++uk; }
+    }
+    if constexpr (VK + 1 < CB)
+      LsqColumns<T, RG, RA, CB, VK + 1>::run(A, gk, uk, la, lb, grg, nrg, W, warp, r, ldm, rowb, part, rdiag,
+                                             dmax, dmin, amin);
+  }
+};
 
 template <typename T, int RG, int RA, int CB, class Asm>
 __global__ void __launch_bounds__(256) k_lsq_mw(LsqArgs<T> a, Asm as, size_t scratch_bytes) {
@@ -36,15 +189,17 @@ __global__ void __launch_bounds__(256) k_lsq_mw(LsqArgs<T> a, Asm as, size_t scr
   const int s = a.s, r = a.r, ldm = r + 1;
   const int la = lane % RG, lb = lane / RG;
   const int grg = warp * RG + la;  // global row group
-  const int NRG = W * RG;
+  const int nrg = W * RG;
   T* Ms = reinterpret_cast<T*>(smem_raw);
   T* Rs = Ms + (size_t)s * ldm;
   T* cvec = Rs + (size_t)r * ldm;
-  T* rowb = cvec + r;                 // 2 x ldm
+  T* rdiag = cvec + r;                // R_kk (beta) per column
+  T* rowb = rdiag + r;                // 2 x ldm
   T* part = rowb + 2 * ldm;           // 2 x W x ldm
-  const size_t core = ((size_t)s * ldm + (size_t)r * ldm + r + 2 * ((size_t)ldm + (size_t)W * ldm)) * sizeof(T);
+  const size_t core =
+      ((size_t)s * ldm + (size_t)r * ldm + 2 * (size_t)r + 2 * ((size_t)ldm + (size_t)W * ldm)) * sizeof(T);
   double* red = reinterpret_cast<double*>(smem_raw + (core + 15) / 16 * 16);  // W doubles (<= 8)
-  unsigned char* scratch = smem_raw + (core + 15) / 16 * 16 + 64 * 2;
+  unsigned char* scratch = smem_raw + (core + 15) / 16 * 16 + 16 * sizeof(double);
   (void)scratch_bytes;
   const CtaGroup grp;
   const double qnan = __longlong_as_double(0x7ff8000000000000ll);
@@ -58,7 +213,7 @@ __global__ void __launch_bounds__(256) k_lsq_mw(LsqArgs<T> a, Asm as, size_t scr
     bool bad = false;
 #pragma unroll
     for (int u = 0; u < RA; ++u) {
-      const int i = grg + NRG * u;
+      const int i = grg + nrg * u;
       const double wi = (i < s && a.w) ? a.w[i] : 1.0;
 #pragma unroll
       for (int v = 0; v < CB; ++v) {
@@ -85,112 +240,34 @@ __global__ void __launch_bounds__(256) k_lsq_mw(LsqArgs<T> a, Asm as, size_t scr
     }
 
     double dmax = 0.0, dmin = DBL_MAX;
-    int amin = 0;
-    for (int k = 0; k < r; ++k) {
-      const int buf = k & 1;
-      T* rk_s = rowb + buf * ldm;
-      T* pt = part + (size_t)buf * W * ldm;
-      const int bk = k % CG, vk = k / CG;
-      const int gk = k % NRG, uk = k / NRG;
-      // x_i = M_ik for own rows (column group bk of this warp, slot vk)
-      T x[RA];
-#pragma unroll
-      for (int u = 0; u < RA; ++u) {
-        T mine = A[u][0];
-#pragma unroll
-        for (int v = 1; v < CB; ++v)
-          if (v == vk) mine = A[u][v];
-        x[u] = shfl_t(mine, la + RG * bk);
-      }
-      // the owner of row k publishes it (columns >= k)
-      if (grg == gk) {
-#pragma unroll
-        for (int u = 0; u < RA; ++u)
-          if (u == uk) {
-#pragma unroll
-            for (int v = 0; v < CB; ++v) {
-              const int j = lb + CG * v;
-              if (j >= k && j <= r) rk_s[j] = A[u][v];
-            }
-          }
-      }
-      // partial Gram row: own rows, butterfly over the warp's row groups
-#pragma unroll
-      for (int v = 0; v < CB; ++v) {
-        T acc = S::zero();
-#pragma unroll
-        for (int u = 0; u < RA; ++u) {
-          const int i = grg + NRG * u;
-          if (i >= k && i < s) acc = S::fma_conj(x[u], A[u][v], acc);
-        }
-#pragma unroll
-        for (int off = 1; off < RG; off <<= 1) acc = S::add(acc, shfl_xor_t(acc, off));
-        const int j = lb + CG * v;
-        if (la == 0 && j >= k && j <= r) pt[warp * ldm + j] = acc;
-      }
-      __syncthreads();
-      double gkk = 0.0;
-      for (int w = 0; w < W; ++w) gkk += S::re(pt[w * ldm + k]);
-      const T alpha = rk_s[k];
-      const double nrm = sqrt(gkk);
-      const double aa = S::abs(alpha);
-      T beta;
-      double tau;
-      if (nrm == 0.0) {
-        beta = S::zero();
-        tau = 0.0;
-      } else {
-        beta = (aa == 0.0) ? S::from(-nrm, 0.0) : S::mulr(alpha, -nrm / aa);
-        tau = 1.0 / (nrm * (nrm + aa));  // 2 / (v^H v)
-      }
-      dmax = fmax(dmax, nrm);
-      if (nrm < dmin) { dmin = nrm; amin = k; }
-      T sj[CB];
-#pragma unroll
-      for (int v = 0; v < CB; ++v) {
-        const int j = lb + CG * v;
-        sj[v] = S::zero();
-        if (j > k && j <= r) {
-          T g = S::zero();
-          for (int w = 0; w < W; ++w) g = S::add(g, pt[w * ldm + j]);
-          sj[v] = S::mulr(S::sub(g, S::mul(S::conj(beta), rk_s[j])), tau);
-        }
-      }
-      const T vdiag = S::sub(alpha, beta);
-#pragma unroll
-      for (int u = 0; u < RA; ++u) {
-        const int i = grg + NRG * u;
-        if (i >= k && i < s) {
-          const T vi = (i == k) ? vdiag : x[u];
-#pragma unroll
-          for (int v = 0; v < CB; ++v) {
-            const int j = lb + CG * v;
-            if (j > k && j <= r) A[u][v] = S::fms(vi, sj[v], A[u][v]);
-            else if (j == k && i == k) A[u][v] = beta;
-          }
-        }
-      }
-    }
+    int amin = 0, gk = 0, uk = 0;
+    LsqColumns<T, RG, RA, CB, 0>::run(A, gk, uk, la, lb, grg, nrg, W, warp, r, ldm, rowb, part, rdiag, dmax,
+                                      dmin, amin);
 
-    // R and y to shared memory, back substitution by warp 0
+    // R (strict upper part from registers, diagonal = beta) and y to shared memory
 #pragma unroll
     for (int u = 0; u < RA; ++u) {
-      const int i = grg + NRG * u;
+      const int i = grg + nrg * u;
 #pragma unroll
       for (int v = 0; v < CB; ++v) {
         const int j = lb + CG * v;
-        if (i < r && j >= i && j <= r) Rs[i * ldm + j] = A[u][v];
+        if (i < r && j > i && j <= r) Rs[i * ldm + j] = A[u][v];
       }
     }
     __syncthreads();
     const bool rankdef = (r > 0) && (dmin < 1e-12 * fmax(dmax, DBL_MIN));
     if (warp == 0) {
       if (!rankdef) {
+        // reciprocals of the diagonal in parallel, then a column sweep
+        const T one = S::from(1.0, 0.0);
+        const T rinv0 = (lane < r) ? S::div(one, rdiag[lane]) : S::zero();
+        const T rinv1 = (lane + 32 < r) ? S::div(one, rdiag[lane + 32]) : S::zero();
         T y0 = (lane < r) ? Rs[lane * ldm + r] : S::zero();
         T y1 = (lane + 32 < r) ? Rs[(lane + 32) * ldm + r] : S::zero();
         for (int k = r - 1; k >= 0; --k) {
-          const T yk = shfl_t(k < 32 ? y0 : y1, k & 31);
-          const T ck = S::div(yk, Rs[k * ldm + k]);
+          const bool lo = k < 32;
+          T ck = S::mul(lo ? y0 : y1, lo ? rinv0 : rinv1);
+          ck = shfl_t(ck, k & 31);
           if (lane == 0) cvec[k] = ck;
           if (lane < k) y0 = S::fms(Rs[lane * ldm + k], ck, y0);
           if (lane + 32 < k) y1 = S::fms(Rs[(lane + 32) * ldm + k], ck, y1);
@@ -200,6 +277,7 @@ __global__ void __launch_bounds__(256) k_lsq_mw(LsqArgs<T> a, Asm as, size_t scr
       }
     }
     __syncthreads();
+    // sampled residual ||w (M c - t)|| from the unweighted M (online.py:121-124)
     double ss = 0.0;
     for (int i = threadIdx.x; i < s; i += blockDim.x) {
       T acc = S::zero();

@@ -16,7 +16,6 @@
 #include "../../include/sas.h"
 #include "sas_common.cuh"
 #include "k_lsq.cuh"
-#include "k_lsq_warp.cuh"
 #include "k_lsq_mw.cuh"
 #include "k_gauss.cuh"
 #include "k_recon.cuh"
@@ -481,31 +480,6 @@ static int launch_lsq_t(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t
   return SAS_OK;
 }
 
-template <typename T, int RA, int CB, class Asm>
-static int launch_lsq_warp_t(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t scratch, cudaStream_t st) {
-  constexpr int kWarps = 2;  // parameter values per CTA (one per warp)
-  const size_t smem = kWarps * lsq_warp_smem_per_warp<T>(a.s, a.r, scratch);
-  auto kern = k_lsq_warp<T, RA, CB, Asm>;
-  SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-  int occ = 0;
-  SAS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * kWarps, smem));
-  if (occ < 1) {
-    sas_set_error("least-squares warp kernel does not fit (s=%d r=%d smem=%zu)", a.s, a.r, smem);
-    return SAS_ERR_ARG;
-  }
-  int64_t grid = (int64_t)occ * pl->sms;
-  const int64_t need = (a.P + kWarps - 1) / kWarps;
-  if (grid > need) grid = need;
-  if (grid < 1) grid = 1;
-  stage_begin(pl, st, SAS_STAGE_LSQ);
-  kern<<<(unsigned)grid, 32 * kWarps, smem, st>>>(a, as, scratch);
-  stage_end(pl, st);
-  SAS_CUDA_CHECK(cudaGetLastError());
-  pl->last_launches++;
-  return SAS_OK;
-}
-
 template <typename T, int RG, int RA, int CB, class Asm>
 static int launch_lsq_mw_t(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t scratch, cudaStream_t st) {
   const int W = (a.s + RG * RA - 1) / (RG * RA);
@@ -534,15 +508,6 @@ static int launch_lsq_mw_t(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, siz
   return SAS_OK;
 }
 
-static int lsq_ra_pref() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SAS_LSQ_RA");
-    v = e ? atoi(e) : 0;
-  }
-  return v;
-}
-
 static bool lsq_force_cta() {
   static int v = -1;
   if (v < 0) {
@@ -552,55 +517,28 @@ static bool lsq_force_cta() {
   return v == 1;
 }
 
-// Kernel choice for the batched least squares (all three compute the same
-// Householder LS, they differ in how many warps share one parameter value):
-//   k_lsq_warp  one warp per p, [M_w | t_w] in one warp's registers (small s, r)
-//   k_lsq_mw    W <= 8 warps per p, registers + one CTA barrier per column step
-//   k_lsq       CTA per p fallback (s up to 512)
-// SAS_LSQ_KERNEL=cta forces the fallback; SAS_LSQ_RA=4 picks the 4-row variant
-// of k_lsq_mw (tuning).
+// Kernel choice for the batched least squares: k_lsq_mw with W warps per
+// parameter value and an (RG row groups x 32/RG column groups) lane layout
+// holding RA x CB register slots per lane; W = ceil(s / (RG*RA)) <= 8.  Small
+// problems run one warp per parameter value (W = 1).  k_lsq (CTA per p,
+// shared-memory Gram partials) is the fallback for shapes outside the table;
+// SAS_LSQ_KERNEL=cta forces it (A/B checks).
 template <typename T, class Asm>
 static int launch_lsq(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t scratch, cudaStream_t st) {
-  const int cols = a.r + 1;
+  const int cols = a.r + 1, s = a.s;
   constexpr bool real = std::is_same<T, double>::value;
   if (!lsq_force_cta()) {
     if (real) {
-      if (cols <= 12) {
-        if (a.s <= 24) return launch_lsq_warp_t<T, 3, 3>(pl, a, as, scratch, st);
-        if (a.s <= 40) return launch_lsq_warp_t<T, 5, 3>(pl, a, as, scratch, st);
-        if (a.s <= 80) return launch_lsq_warp_t<T, 10, 3>(pl, a, as, scratch, st);
-        if (a.s <= 128) return launch_lsq_warp_t<T, 16, 3>(pl, a, as, scratch, st);
-      } else if (cols <= 24) {
-        if (a.s <= 40) return launch_lsq_warp_t<T, 5, 6>(pl, a, as, scratch, st);
-        if (a.s <= 80) return launch_lsq_warp_t<T, 10, 6>(pl, a, as, scratch, st);
-      } else if (cols <= 32) {
-        if (a.s <= 40) return launch_lsq_warp_t<T, 5, 8>(pl, a, as, scratch, st);
-      }
+      if (cols <= 12 && s <= 24) return launch_lsq_mw_t<T, 8, 3, 3>(pl, a, as, scratch, st);
+      if (cols <= 12 && s <= 640) return launch_lsq_mw_t<T, 8, 10, 3>(pl, a, as, scratch, st);
+      if (cols <= 24 && s <= 640) return launch_lsq_mw_t<T, 8, 10, 6>(pl, a, as, scratch, st);
+      if (cols <= 32 && s <= 256) return launch_lsq_mw_t<T, 4, 8, 4>(pl, a, as, scratch, st);
+      if (cols <= 48 && s <= 256) return launch_lsq_mw_t<T, 4, 8, 6>(pl, a, as, scratch, st);
+      if (cols <= 64 && s <= 256) return launch_lsq_mw_t<T, 4, 8, 8>(pl, a, as, scratch, st);
     } else {
-      if (cols <= 12 && a.s <= 24) return launch_lsq_warp_t<T, 3, 3>(pl, a, as, scratch, st);
-      if (cols <= 12 && a.s <= 40) return launch_lsq_warp_t<T, 5, 3>(pl, a, as, scratch, st);
-    }
-    const bool ra4 = lsq_ra_pref() == 4;
-    if (real) {
-      // RG = 4 row groups x 8 column groups per warp
-      if (ra4 && a.s <= 128) {
-        if (cols <= 32) return launch_lsq_mw_t<T, 4, 4, 4>(pl, a, as, scratch, st);
-        if (cols <= 48) return launch_lsq_mw_t<T, 4, 4, 6>(pl, a, as, scratch, st);
-        return launch_lsq_mw_t<T, 4, 4, 8>(pl, a, as, scratch, st);
-      }
-      if (a.s <= 256) {
-        if (cols <= 32) return launch_lsq_mw_t<T, 4, 8, 4>(pl, a, as, scratch, st);
-        if (cols <= 48) return launch_lsq_mw_t<T, 4, 8, 6>(pl, a, as, scratch, st);
-        return launch_lsq_mw_t<T, 4, 8, 8>(pl, a, as, scratch, st);
-      }
-    } else {
-      // complex: RG = 8 x 4 column groups for narrow bases, 4 x 8 otherwise
-      if (cols <= 12) {
-        if (ra4 && a.s <= 256) return launch_lsq_mw_t<T, 8, 4, 3>(pl, a, as, scratch, st);
-        if (a.s <= 512) return launch_lsq_mw_t<T, 8, 8, 3>(pl, a, as, scratch, st);
-      } else if (cols <= 32 && a.s <= 256) {
-        return launch_lsq_mw_t<T, 4, 8, 4>(pl, a, as, scratch, st);
-      }
+      if (cols <= 12 && s <= 24) return launch_lsq_mw_t<T, 8, 3, 3>(pl, a, as, scratch, st);
+      if (cols <= 12 && s <= 512) return launch_lsq_mw_t<T, 8, 8, 3>(pl, a, as, scratch, st);
+      if (cols <= 32 && s <= 256) return launch_lsq_mw_t<T, 4, 8, 4>(pl, a, as, scratch, st);
     }
   }
   if (cols <= 32) {
