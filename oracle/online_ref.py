@@ -128,18 +128,27 @@ def relative_residual(a_matrix, x, b):
     return float(np.linalg.norm(a_matrix @ x - b) / max(np.linalg.norm(b), 1e-300))
 
 
-def ls_floor(m, tb, weights, draws=4, seed=0):
+def ls_floor(m, tb, weights, draws=4, seed=0, rows=None, basis=None, inverse=None):
     """Parity floor of the LS solution at one parameter: relative spread of the
-    solution under 1-ulp relative perturbations of the (weighted) data, i.e.
-    how far two valid fp64 evaluations can disagree."""
+    solution under 1-ulp relative perturbations of the data, i.e. how far two
+    valid fp64 evaluations can disagree.  For row-oracle
+    systems pass the operator rows (dense, unique rows), the basis and the
+    inverse map: the perturbation is then applied to the row entries before the
+    contraction with X, which is where the cancellation of stencil rows
+    (diagonal ~ sum of off-diagonals) amplifies rounding."""
     rng = np.random.default_rng(seed)
     base = solve_ls(m, tb, weights=weights)
     nb = max(np.linalg.norm(base), 1e-300)
     worst = 0.0
     eps = np.finfo(float).eps
     for _ in range(draws):
-        dm = 1.0 + eps * rng.choice([-1.0, 1.0], size=m.shape)
         dt = 1.0 + eps * rng.choice([-1.0, 1.0], size=tb.shape)
-        c = solve_ls(m * dm, tb * dt, weights=weights)
+        if rows is not None:
+            rr = np.asarray(rows.toarray() if hasattr(rows, "toarray") else rows)
+            dr = 1.0 + eps * rng.choice([-1.0, 1.0], size=rr.shape)
+            mp = np.asarray((rr * dr) @ basis)[inverse]
+        else:
+            mp = m * (1.0 + eps * rng.choice([-1.0, 1.0], size=m.shape))
+        c = solve_ls(mp, tb * dt, weights=weights)
         worst = max(worst, np.linalg.norm(c - base) / nb)
     return worst

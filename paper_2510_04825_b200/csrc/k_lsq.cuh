@@ -70,6 +70,23 @@ struct WarpGroup {
   __device__ __forceinline__ void sync() const { __syncwarp(); }
 };
 
+// (i, j) walk over an s x r matrix in row-major order, stepping `step` entries
+// per iteration without a division per element.
+struct RowMajorWalk {
+  int i, j, di, dj, r;
+  __device__ __forceinline__ RowMajorWalk(int start, int step, int r_) : r(r_) {
+    i = start / r_;
+    j = start - i * r_;
+    di = step / r_;
+    dj = step - di * r_;
+  }
+  __device__ __forceinline__ void next() {
+    i += di;
+    j += dj;
+    if (j >= r) { j -= r; ++i; }
+  }
+};
+
 // ---------------------------------------------------------------------------
 template <typename T>
 struct AsmGlobal {
@@ -79,10 +96,8 @@ struct AsmGlobal {
   __device__ __forceinline__ void operator()(const Grp& g, int64_t p, T* Ms, int ldm, int s, int r,
                                              unsigned char*) const {
     const T* src = M + p * (int64_t)s * r;
-    for (int idx = g.rank(); idx < s * r; idx += g.size()) {
-      int i = idx / r, j = idx - i * r;
-      Ms[i * ldm + j] = src[idx];
-    }
+    RowMajorWalk wk(g.rank(), g.size(), r);
+    for (int idx = g.rank(); idx < s * r; idx += g.size(), wk.next()) Ms[wk.i * ldm + wk.j] = src[idx];
   }
 };
 
@@ -146,24 +161,28 @@ struct AsmAffine {
     }
     g.sync();
     const int64_t blk = (int64_t)s * r;
-    for (int idx = g.rank(); idx < s * r; idx += g.size()) {
-      int i = idx / r, j = idx - i * r;
+    RowMajorWalk wk(g.rank(), g.size(), r);
+    for (int idx = g.rank(); idx < s * r; idx += g.size(), wk.next()) {
       // m = f0*B0; m = m + fk*Bk  (online.py:110-112, numpy elementwise order)
       T m = Sc<T>::mul_exact(f[0], blocks[idx]);
       for (int k = 1; k < K; ++k) m = Sc<T>::add_exact(m, Sc<T>::mul_exact(f[k], blocks[k * blk + idx]));
-      Ms[i * ldm + j] = m;
+      Ms[wk.i * ldm + wk.j] = m;
     }
   }
 };
 
 // Edge-form stencil rows (real).  Row i of A(p) for node S_i:
 //   c_e = exp(sum_k p_k phi[i][e][k]) / hh      (sequential sum, no FMA)
-//   diag = sum_e c_e (edge order), off-diagonal -c_e for interior neighbours.
-// G[i][0] = X[S_i], G[i][1+e] = X[nbr_e] (zero rows for boundary edges).
+//   diag = sum_e c_e (edge order), off-diagonal -c_e for interior neighbours
+// (the harness row oracle, oracle/online_ref.py stencil_rows).  The product
+// with X accumulates the row's nonzeros in ascending column order with FMA,
+// as the reference's dense rows_dense(...) @ basis does (online.py:62):
+//   G[i][q] = X[node_q], gmap[i][q] = 0 (diagonal) | 1+e (edge e) | -1 (pad).
 struct AsmStencil {
   int E, dp;
-  const double* phi;   // s x E x dp
-  const double* G;     // s x (E+1) x r
+  const double* phi;    // s x E x dp
+  const double* G;      // s x (E+1) x r
+  const int8_t* gmap;   // s x (E+1)
   double hh;
   const double* params;  // P x dp (real)
   static size_t scratch_bytes(int s, int E) { return (size_t)s * (E + 1) * sizeof(double); }
@@ -173,25 +192,32 @@ struct AsmStencil {
     double* cs = reinterpret_cast<double*>(scratch);
     const double* pp = params + p * dp;
     const int E1 = E + 1;
-    for (int idx = g.rank(); idx < s * E; idx += g.size()) {
-      int i = idx / E, e = idx - i * E;
-      const double* ph = phi + (int64_t)idx * dp;
-      double arg = dmul_exact(pp[0], ph[0]);
-      for (int k = 1; k < dp; ++k) arg = dadd_exact(arg, dmul_exact(pp[k], ph[k]));
-      cs[i * E1 + 1 + e] = exp(arg) / hh;
-    }
-    g.sync();
+    // one row per thread: edge coefficients and the diagonal (edge order)
     for (int i = g.rank(); i < s; i += g.size()) {
       double d = 0.0;
-      for (int e = 0; e < E; ++e) d = dadd_exact(d, cs[i * E1 + 1 + e]);
+      for (int e = 0; e < E; ++e) {
+        const double* ph = phi + ((int64_t)i * E + e) * dp;
+        double arg = dmul_exact(pp[0], ph[0]);
+        for (int k = 1; k < dp; ++k) arg = dadd_exact(arg, dmul_exact(pp[k], ph[k]));
+        const double c = exp(arg) / hh;
+        cs[i * E1 + 1 + e] = c;
+        d = dadd_exact(d, c);
+      }
       cs[i * E1] = d;
     }
     g.sync();
-    for (int idx = g.rank(); idx < s * r; idx += g.size()) {
-      int i = idx / r, j = idx - i * r;
-      const double* g = G + (int64_t)i * E1 * r + j;
-      double m = cs[i * E1] * g[0];
-      for (int e = 0; e < E; ++e) m = fma(-cs[i * E1 + 1 + e], g[(1 + e) * r], m);
+    RowMajorWalk wk(g.rank(), g.size(), r);
+    for (int idx = g.rank(); idx < s * r; idx += g.size(), wk.next()) {
+      const int i = wk.i, j = wk.j;
+      const double* gr = G + (int64_t)i * E1 * r + j;
+      const int8_t* mp = gmap + i * E1;
+      double m = 0.0;
+      for (int q = 0; q < E1; ++q) {
+        const int slot = mp[q];
+        if (slot < 0) break;
+        const double a = (slot == 0) ? cs[i * E1] : -cs[i * E1 + slot];
+        m = fma(a, gr[q * r], m);
+      }
       Ms[i * ldm + j] = m;
     }
   }

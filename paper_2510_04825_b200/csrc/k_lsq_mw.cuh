@@ -20,8 +20,9 @@
 // Householder step k, Gram-row formulation (one reduction per column):
 //   x_i = M_ik            shuffle from column group k mod CG of the same rows
 //   g_j = sum_i conj(x_i) M_ij    own rows, butterfly over the warp's RG row
-//                         groups, warp partials in shared memory, ONE barrier,
-//                         every thread sums the W partials in warp order
+//                         groups, warp partials in shared memory; after a
+//                         barrier one thread per column sums the W partials in
+//                         warp order (a second barrier publishes the totals)
 //   |x| = sqrt(g_kk), beta = -e^{i arg M_kk} |x|, tau = 2 / v^H v
 //   M_ij -= tau v_i (g_j - conj(beta) M_kj)      for j > k
 // The column loop is split as k = bk + CG*vk with the slot vk unrolled, so the
@@ -116,8 +117,16 @@ struct LsqStep {
       if (la == 0 && j >= k && j <= r) pt[warp * ldm + j] = acc;
     }
     __syncthreads();
-    double gkk = 0.0;
-    for (int w = 0; w < W; ++w) gkk += S::re(pt[w * ldm + k]);
+    // column totals of the W warp partials, once per column (fixed warp order)
+    if (W > 1) {
+      for (int j = k + threadIdx.x; j <= r; j += blockDim.x) {
+        T g = pt[j];
+        for (int w = 1; w < W; ++w) g = S::add(g, pt[w * ldm + j]);
+        pt[j] = g;
+      }
+      __syncthreads();
+    }
+    const double gkk = S::re(pt[k]);
     const T alpha = rk_s[k];
     const double nrm = sqrt(gkk);
     const double aa = S::abs(alpha);
@@ -137,12 +146,7 @@ struct LsqStep {
 #pragma unroll
     for (int v = VK; v < CB; ++v) {
       const int j = lb + CG * v;
-      sj[v] = S::zero();
-      if (j > k && j <= r) {
-        T g = S::zero();
-        for (int w = 0; w < W; ++w) g = S::add(g, pt[w * ldm + j]);
-        sj[v] = S::mulr(S::sub(g, S::mul(S::conj(beta), rk_s[j])), tau);
-      }
+      sj[v] = (j > k && j <= r) ? S::mulr(S::sub(pt[j], S::mul(S::conj(beta), rk_s[j])), tau) : S::zero();
     }
     // v_i: x_i below the diagonal, alpha - beta on it, 0 above
     const T vdiag = S::sub(alpha, beta);

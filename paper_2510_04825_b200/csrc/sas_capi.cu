@@ -10,6 +10,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <algorithm>
 #include <type_traits>
 #include <vector>
 
@@ -106,7 +107,8 @@ struct sas_plan {
   // stencil
   int E = 0;
   double* phi = nullptr;
-  double* G = nullptr;
+  double* G = nullptr;     // s x (E+1) x r gathered basis rows, ascending node order per row
+  int8_t* gmap = nullptr;  // s x (E+1) coefficient slot of each gathered row
   double hh = 1.0;
   // gauss
   double* pts = nullptr;
@@ -199,7 +201,7 @@ static void plan_free(sas_plan* pl) {
   if (!pl) return;
   DevGuard g(pl->device);
   void* ptrs[] = {pl->X, pl->S, pl->w, pl->t, pl->proj, pl->kind, pl->scale, pl->rate, pl->blocks,
-                  pl->phi, pl->G, pl->pts, pl->D, pl->Dfrag, pl->Xfrag, pl->full_nbr, pl->full_phi, pl->full_b,
+                  pl->phi, pl->G, pl->gmap, pl->pts, pl->D, pl->Dfrag, pl->Xfrag, pl->full_nbr, pl->full_phi, pl->full_b,
                   pl->csr_rp_d, pl->csr_ci_d, pl->csr_va_d, pl->Mscr, pl->rpart, pl->fco,
                   pl->h_params, pl->h_ctab, pl->h_rhs, pl->h_coef, pl->h_sres, pl->h_outv,
                   pl->h_status, pl->h_bad};
@@ -214,16 +216,16 @@ static void plan_free(sas_plan* pl) {
   delete pl;
 }
 
-__global__ void k_stencil_gather(const double* __restrict__ X, int r, const int64_t* __restrict__ S,
-                                 const int64_t* __restrict__ nbr, int s, int E, double* __restrict__ G) {
+// G[i][q] = X[gidx[i][q]] (zero row for gidx < 0): the stencil row's nodes in
+// ascending column order, the order a dense row times X accumulates them in.
+__global__ void k_stencil_gather(const double* __restrict__ X, int r, const int64_t* __restrict__ gidx, int s,
+                                 int E1, double* __restrict__ G) {
   int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t tot = (int64_t)s * (E + 1) * r;
+  int64_t tot = (int64_t)s * E1 * r;
   if (idx >= tot) return;
   int j = (int)(idx % r);
-  int64_t ie = idx / r;
-  int e1 = (int)(ie % (E + 1));
-  int i = (int)(ie / (E + 1));
-  int64_t node = (e1 == 0) ? S[i] : nbr[(int64_t)i * E + e1 - 1];
+  int64_t iq = idx / r;
+  int64_t node = gidx[iq];
   G[idx] = (node >= 0) ? X[node * r + j] : 0.0;
 }
 
@@ -346,14 +348,33 @@ extern "C" int sas_plan_create(const sas_desc* desc, const void* X, int64_t n, i
       pl->E = desc->n_edges;
       pl->hh = desc->edge_div;
       TRY(dupload(&pl->phi, desc->edge_phi, (size_t)s * pl->E * pl->dp * sizeof(double)));
-      int64_t* nbr_d = nullptr;
-      TRY(dupload(&nbr_d, desc->edge_nbr, (size_t)s * pl->E * sizeof(int64_t)));
-      rc = dalloc(&pl->G, (size_t)s * (pl->E + 1) * r * sizeof(double));
-      if (rc) { cudaFree(nbr_d); plan_free(pl); return rc; }
-      int64_t tot = (int64_t)s * (pl->E + 1) * r;
-      k_stencil_gather<<<(unsigned)((tot + 255) / 256), 256>>>((const double*)pl->X, r, pl->S, nbr_d, s, pl->E, pl->G);
+      // per selected row: its nodes (diagonal S_i and interior neighbours) in
+      // ascending node order; gmap[q] = 0 for the diagonal, 1+e for edge e, -1 pad
+      const int E1 = pl->E + 1;
+      std::vector<int64_t> gidx((size_t)s * E1, -1);
+      std::vector<int8_t> gmap((size_t)s * E1, -1);
+      for (int i = 0; i < s; ++i) {
+        std::vector<std::pair<int64_t, int>> ent;
+        ent.emplace_back(S[i], 0);
+        for (int e = 0; e < pl->E; ++e) {
+          const int64_t m = desc->edge_nbr[(int64_t)i * pl->E + e];
+          if (m >= 0) ent.emplace_back(m, 1 + e);
+        }
+        std::sort(ent.begin(), ent.end());
+        for (size_t q = 0; q < ent.size(); ++q) {
+          gidx[(size_t)i * E1 + q] = ent[q].first;
+          gmap[(size_t)i * E1 + q] = (int8_t)ent[q].second;
+        }
+      }
+      int64_t* gidx_d = nullptr;
+      TRY(dupload(&gidx_d, gidx.data(), gidx.size() * sizeof(int64_t)));
+      TRY(dupload(&pl->gmap, gmap.data(), gmap.size()));
+      rc = dalloc(&pl->G, (size_t)s * E1 * r * sizeof(double));
+      if (rc) { cudaFree(gidx_d); plan_free(pl); return rc; }
+      int64_t tot = (int64_t)s * E1 * r;
+      k_stencil_gather<<<(unsigned)((tot + 255) / 256), 256>>>((const double*)pl->X, r, gidx_d, s, E1, pl->G);
       cudaError_t e = cudaDeviceSynchronize();
-      cudaFree(nbr_d);
+      cudaFree(gidx_d);
       if (e != cudaSuccess) { plan_free(pl); sas_set_error("stencil gather: %s", cudaGetErrorString(e)); return SAS_ERR_CUDA; }
       break;
     }
@@ -638,7 +659,7 @@ static int solve_t(sas_plan* pl, const void* params, int64_t P, const double* co
     }
     case SAS_OP_STENCIL: {
       if constexpr (std::is_same<T, double>::value) {
-        AsmStencil as{pl->E, pl->dp, pl->phi, pl->G, pl->hh, (const double*)params};
+        AsmStencil as{pl->E, pl->dp, pl->phi, pl->G, pl->gmap, pl->hh, (const double*)params};
         return launch_lsq<double>(pl, a, as, AsmStencil::scratch_bytes(pl->s, pl->E), st);
       }
       sas_set_error("stencil: complex not supported");

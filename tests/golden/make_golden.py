@@ -119,9 +119,12 @@ def run_reference(rsys, points, mode, samples, seed, params, strategy="leverage"
         # parity floor from the reference's own M at this p
         if plan.affine:
             m = sum(t.coeff(p) * blk for t, blk in zip(rsys.affine_terms, plan.blocks))
+            floors.append(online_ref.ls_floor(m, rsys.rhs(p, selector.indices), selector.weights))
         else:
             m = ref_online._sampled_rows(rsys, basis, selector.indices, p)
-        floors.append(online_ref.ls_floor(m, rsys.rhs(p, selector.indices), selector.weights))
+            uniq, inverse = np.unique(selector.indices, return_inverse=True)
+            floors.append(online_ref.ls_floor(m, rsys.rhs(p, selector.indices), selector.weights,
+                                              rows=rsys.rows_dense(p, uniq), basis=basis.basis, inverse=inverse))
     return dict(
         X=np.asarray(basis.basis), S=np.asarray(selector.indices, dtype=np.int64),
         w=np.asarray(selector.weights) if selector.weights is not None else np.zeros(0),

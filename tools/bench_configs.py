@@ -59,16 +59,19 @@ def oracle_coef(prob, basis, sel, p):
         blocks = online_ref.affine_blocks([t.matrix for t in sysm.affine_terms], X, idx)
         coeffs = [complex(t.scale) if t.kind == "const" else complex(t.scale) * p for t in sysm.affine_terms]
         m = online_ref.affine_combine(coeffs, blocks)
-    elif isinstance(sysm.operator, GaussianKernelOperator):
-        op = sysm.operator
-        m = online_ref.sampled_rows(lambda q, rows: online_ref.gauss_rows(op.points, rows, float(q), op.ridge),
-                                    X, idx, p)
+        t = sysm.rhs(p, idx)
+        c, sres, _ = online_ref.solve_one(m, t, sel.weights)
+        return c, sres, online_ref.ls_floor(m, t, sel.weights, draws=2)
+    op = sysm.operator
+    if isinstance(op, GaussianKernelOperator):
+        fn = lambda q, rows: online_ref.gauss_rows(op.points, rows, float(q), op.ridge)
     else:
-        op = sysm.operator
-        m = online_ref.sampled_rows(lambda q, rows: online_ref.stencil_rows(op, q, rows), X, idx, p)
+        fn = lambda q, rows: online_ref.stencil_rows(op, q, rows)
+    m = online_ref.sampled_rows(fn, X, idx, p)
     t = sysm.rhs(p, idx)
     c, sres, _ = online_ref.solve_one(m, t, sel.weights)
-    floor = online_ref.ls_floor(m, t, sel.weights, draws=2)
+    uniq, inverse = np.unique(idx, return_inverse=True)
+    floor = online_ref.ls_floor(m, t, sel.weights, draws=2, rows=fn(p, uniq), basis=X, inverse=inverse)
     return c, sres, floor
 
 
