@@ -146,3 +146,51 @@ def test_empty_batch():
     assert online.solve_batch(plan, []) == []
     res = online.solve_params(plan, [])
     assert res.coefficients.shape == (0, case.basis.rank)
+
+
+class _RefLikeTerm:
+    """Duck-typed stand-in for subapsnap.systems.AffineTerm (complex scale,
+    kind 'other' for opaque callables), systems.py:76-100."""
+
+    def __init__(self, coeff, matrix, kind, scale=1.0):
+        self.coeff, self.matrix, self.kind, self.scale = coeff, matrix, kind, scale
+
+
+class _RefLikeSystem:
+    """Duck-typed stand-in for subapsnap.systems.ParametricSystem: opaque
+    coefficient and rhs callables, no GPU descriptor attributes."""
+
+    def __init__(self, base):
+        import cmath
+        self.n = base.n
+        self.domain = base.domain
+        self.output_functional = base.output_functional
+        a1 = base.affine_terms[2].matrix
+        self.affine_terms = (
+            _RefLikeTerm(lambda p, s=complex(1.0): s * p, base.affine_terms[0].matrix, "linear", complex(1.0)),
+            _RefLikeTerm(lambda p, s=complex(-1.0): s, base.affine_terms[1].matrix, "const", complex(-1.0)),
+            _RefLikeTerm(lambda p: -cmath.exp(0.1 * p), a1, "other"),
+        )
+        self._b = base.b
+
+    def rhs(self, p, idx):
+        return self._b[np.asarray(idx)]
+
+    def full_rhs(self, p):
+        return self._b
+
+
+def test_reference_like_system_with_opaque_coefficient():
+    """An opaque coefficient callable (the reference's delay term) goes through
+    the per-p coefficient table; an opaque rhs callable through the rhs table."""
+    case = load("delay")
+    sysm = _RefLikeSystem(case.system)
+    plan = online.precompute_online(sysm, case.basis, case.selector)
+    assert plan.gpu.table_terms == [2]
+    res = online.solve_params(plan, case.params)
+    assert np.all(res.status == 0)
+    assert res.coefficients.dtype == np.complex128
+    ref = case.data["coef"]
+    for k in range(len(case.params)):
+        d = np.linalg.norm(res.coefficients[k] - ref[k]) / np.linalg.norm(ref[k])
+        assert d <= _tol(case, k)
