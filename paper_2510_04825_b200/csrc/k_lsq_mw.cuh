@@ -1,5 +1,5 @@
-// K4: batched weighted least squares, W <= 8 warps cooperating on one
-// parameter value (W = 1 for small problems).  Replaces linalg.solve_ls
+// K4: batched weighted least squares, W warps cooperating on one parameter
+// value (W = 1 for small problems).  Replaces linalg.solve_ls
 // (reference linalg.py:89-113) as called from online.solve_online
 // (online.py:105-134):
 //
@@ -25,9 +25,10 @@
 //                         warp order (a second barrier publishes the totals)
 //   |x| = sqrt(g_kk), beta = -e^{i arg M_kk} |x|, tau = 2 / v^H v
 //   M_ij -= tau v_i (g_j - conj(beta) M_kj)      for j > k
-// The column loop is split as k = bk + CG*vk with the slot vk unrolled, so the
-// register slot of column k is a compile-time index and finished column slots
-// (v < vk) drop out of the unrolled code.  Reductions are in a fixed order:
+// The column loop is split as k = bk + CG*vk with the slot vk unrolled; W is a
+// template parameter and W*RG a multiple of CG, so the register slots of
+// column k and of row k are compile-time indices and finished column and row
+// slots drop out of the unrolled code.  Reductions are in a fixed order:
 // results do not depend on the grid, the batch or the number of GPUs.
 //
 // The assembler functor fills shared memory with the unweighted M(p):
@@ -69,59 +70,63 @@ __device__ __forceinline__ double rcp_nr(double x) {
 }
 
 template <typename T>
-__host__ __device__ inline size_t lsq_mw_smem_bytes(int s, int r, int W, size_t scratch) {
+__host__ __device__ inline size_t lsq_mw_smem_bytes(int s, int r, int W, int CGxCB, size_t scratch) {
   const int ldm = r + 1;
-  // Ms (s x ldm), R/y (r x ldm), c (r), R_kk (r), 2 x [row k (ldm) + partials (W x ldm)]
-  size_t n = (size_t)s * ldm + (size_t)r * ldm + 2 * (size_t)r + 2 * ((size_t)ldm + (size_t)W * ldm);
+  // Ms (s x ldm), R/y (r x ldm), c (r), R_kk (r),
+  // 2 x [row k (CG*CB) + partials (W x CG*CB)]
+  size_t n = (size_t)s * ldm + (size_t)r * ldm + 2 * (size_t)r + 2 * ((size_t)CGxCB + (size_t)W * CGxCB);
   size_t bytes = (n * sizeof(T) + 15) / 16 * 16;
   return bytes + 16 * sizeof(double) + (scratch + 15) / 16 * 16;
 }
 
-template <typename T, int RG, int RA, int CB>
+// One Householder step for column k = bk + CG*VK.  With NRG = W*RG a multiple
+// of CG, the pivot row k lies in row slot UK = VK / (NRG/CG) for every bk, so
+// both the column slot of k and the row slot of row k are compile-time
+// constants: row slots u < UK hold finished R rows (skipped), u > UK hold rows
+// below the pivot, and only slot UK needs a per-lane test.
+template <typename T, int RG, int RA, int CB, int W>
 struct LsqStep {
   using S = Sc<T>;
   static constexpr int CG = 32 / RG;
-  // One Householder step for column k = bk + CG*VK (VK compile-time).
+  static constexpr int NRG = W * RG;
+  static constexpr int LDP = CG * CB;  // padded row length of the shared row/partial buffers
+  static_assert(NRG % CG == 0, "row groups must be a multiple of the column groups");
+
   template <int VK>
-  static __device__ __forceinline__ void run(T (&A)[RA][CB], int k, int bk, int gk, int uk, int la, int lb,
-                                             int grg, int nrg, int W, int warp, int r, int ldm, T* rk_s,
-                                             T* pt, T* rdiag, double& dmax, double& dmin, int& amin) {
-    // x_i = M_ik for own rows; rows above k contribute nothing
+  static __device__ __forceinline__ void run(T (&A)[RA][CB], int k, int bk, int la, int lb, int grg, int warp,
+                                             int r, T* rk_s, T* pt, T* rdiag, double& dmax, double& dmin,
+                                             int& amin) {
+    constexpr int UK = VK / (NRG / CG);
+    const int gk = CG * (VK % (NRG / CG)) + bk;  // row group of row k
+    // x_i = M_ik for own rows from column group bk (static slot VK)
     T xg[RA];
 #pragma unroll
-    for (int u = 0; u < RA; ++u) {
+    for (int u = UK; u < RA; ++u) {
       const T xv = shfl_t(A[u][VK], la + RG * bk);
-      xg[u] = (grg + nrg * u >= k) ? xv : S::zero();
+      xg[u] = (u > UK || grg >= gk) ? xv : S::zero();
     }
-    // owner of row k publishes it
+    // the owner of row k publishes it (static slot UK; the buffer is padded to CG*CB)
     if (grg == gk) {
 #pragma unroll
-      for (int u = 0; u < RA; ++u)
-        if (u == uk) {
-#pragma unroll
-          for (int v = VK; v < CB; ++v) {
-            const int j = lb + CG * v;
-            if (j >= k && j <= r) rk_s[j] = A[u][v];
-          }
-        }
+      for (int v = VK; v < CB; ++v) rk_s[lb + CG * v] = A[UK][v];
     }
-    // Gram row over own rows, butterfly over the RG row groups of the warp
+    // Gram row over rows >= k, butterfly over the RG row groups of the warp
 #pragma unroll
     for (int v = VK; v < CB; ++v) {
       T acc = S::zero();
 #pragma unroll
-      for (int u = 0; u < RA; ++u) acc = S::fma_conj(xg[u], A[u][v], acc);
+      for (int u = UK; u < RA; ++u) acc = S::fma_conj(xg[u], A[u][v], acc);
 #pragma unroll
       for (int off = 1; off < RG; off <<= 1) acc = S::add(acc, shfl_xor_t(acc, off));
-      const int j = lb + CG * v;
-      if (la == 0 && j >= k && j <= r) pt[warp * ldm + j] = acc;
+      if (la == 0) pt[warp * LDP + lb + CG * v] = acc;
     }
     __syncthreads();
-    // column totals of the W warp partials, once per column (fixed warp order)
     if (W > 1) {
+      // column totals of the W warp partials, one thread per column, warp order
       for (int j = k + threadIdx.x; j <= r; j += blockDim.x) {
         T g = pt[j];
-        for (int w = 1; w < W; ++w) g = S::add(g, pt[w * ldm + j]);
+#pragma unroll
+        for (int w = 1; w < W; ++w) g = S::add(g, pt[w * LDP + j]);
         pt[j] = g;
       }
       __syncthreads();
@@ -146,62 +151,59 @@ struct LsqStep {
 #pragma unroll
     for (int v = VK; v < CB; ++v) {
       const int j = lb + CG * v;
-      sj[v] = (j > k && j <= r) ? S::mulr(S::sub(pt[j], S::mul(S::conj(beta), rk_s[j])), tau) : S::zero();
+      const T w = S::mulr(S::sub(pt[j], S::mul(S::conj(beta), rk_s[j])), tau);
+      sj[v] = (v > VK || j > k) ? w : S::zero();  // columns <= k keep their values
     }
-    // v_i: x_i below the diagonal, alpha - beta on it, 0 above
+    // v_i: x_i below the pivot, alpha - beta on it, 0 above
     const T vdiag = S::sub(alpha, beta);
 #pragma unroll
-    for (int u = 0; u < RA; ++u) {
-      const int i = grg + nrg * u;
-      const T vi = (i == k) ? vdiag : xg[u];
+    for (int u = UK; u < RA; ++u) {
+      const T vi = (u == UK && grg == gk) ? vdiag : xg[u];
 #pragma unroll
       for (int v = VK; v < CB; ++v) A[u][v] = S::fms(vi, sj[v], A[u][v]);
     }
   }
 };
 
-template <typename T, int RG, int RA, int CB, int VK>
+template <typename T, int RG, int RA, int CB, int W, int VK>
 struct LsqColumns {
-  static __device__ __forceinline__ void run(T (&A)[RA][CB], int& gk, int& uk, int la, int lb, int grg, int nrg,
-                                             int W, int warp, int r, int ldm, T* rowb, T* part, T* rdiag,
-                                             double& dmax, double& dmin, int& amin) {
+  static __device__ __forceinline__ void run(T (&A)[RA][CB], int la, int lb, int grg, int warp, int r, T* rowb,
+                                             T* part, T* rdiag, double& dmax, double& dmin, int& amin) {
     constexpr int CG = 32 / RG;
+    constexpr int LDP = CG * CB;
     if (VK * CG >= r) return;
 #pragma unroll 1
     for (int bk = 0; bk < CG; ++bk) {
       const int k = bk + CG * VK;
       if (k >= r) break;
       const int buf = k & 1;
-      LsqStep<T, RG, RA, CB>::template run<VK>(A, k, bk, gk, uk, la, lb, grg, nrg, W, warp, r, ldm,
-                                               rowb + buf * ldm, part + (size_t)buf * W * ldm, rdiag, dmax,
-                                               dmin, amin);
-      if (++gk == nrg) { gk = 0; ++uk; }
+      LsqStep<T, RG, RA, CB, W>::template run<VK>(A, k, bk, la, lb, grg, warp, r, rowb + buf * LDP,
+                                                  part + (size_t)buf * W * LDP, rdiag, dmax, dmin, amin);
     }
     if constexpr (VK + 1 < CB)
-      LsqColumns<T, RG, RA, CB, VK + 1>::run(A, gk, uk, la, lb, grg, nrg, W, warp, r, ldm, rowb, part, rdiag,
-                                             dmax, dmin, amin);
+      LsqColumns<T, RG, RA, CB, W, VK + 1>::run(A, la, lb, grg, warp, r, rowb, part, rdiag, dmax, dmin, amin);
   }
 };
 
-template <typename T, int RG, int RA, int CB, class Asm>
-__global__ void __launch_bounds__(256) k_lsq_mw(LsqArgs<T> a, Asm as, size_t scratch_bytes) {
+template <typename T, int RG, int RA, int CB, int W, class Asm>
+__global__ void __launch_bounds__(32 * W) k_lsq_mw(LsqArgs<T> a, Asm as, size_t scratch_bytes) {
   using S = Sc<T>;
   constexpr int CG = 32 / RG;
+  constexpr int LDP = CG * CB;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int W = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int s = a.s, r = a.r, ldm = r + 1;
   const int la = lane % RG, lb = lane / RG;
   const int grg = warp * RG + la;  // global row group
-  const int nrg = W * RG;
+  constexpr int nrg = W * RG;
   T* Ms = reinterpret_cast<T*>(smem_raw);
   T* Rs = Ms + (size_t)s * ldm;
   T* cvec = Rs + (size_t)r * ldm;
   T* rdiag = cvec + r;                // R_kk (beta) per column
-  T* rowb = rdiag + r;                // 2 x ldm
-  T* part = rowb + 2 * ldm;           // 2 x W x ldm
+  T* rowb = rdiag + r;                // 2 x LDP
+  T* part = rowb + 2 * LDP;           // 2 x W x LDP
   const size_t core =
-      ((size_t)s * ldm + (size_t)r * ldm + 2 * (size_t)r + 2 * ((size_t)ldm + (size_t)W * ldm)) * sizeof(T);
+      ((size_t)s * ldm + (size_t)r * ldm + 2 * (size_t)r + 2 * ((size_t)LDP + (size_t)W * LDP)) * sizeof(T);
   double* red = reinterpret_cast<double*>(smem_raw + (core + 15) / 16 * 16);  // W doubles (<= 8)
   unsigned char* scratch = smem_raw + (core + 15) / 16 * 16 + 16 * sizeof(double);
   (void)scratch_bytes;
@@ -244,9 +246,8 @@ __global__ void __launch_bounds__(256) k_lsq_mw(LsqArgs<T> a, Asm as, size_t scr
     }
 
     double dmax = 0.0, dmin = DBL_MAX;
-    int amin = 0, gk = 0, uk = 0;
-    LsqColumns<T, RG, RA, CB, 0>::run(A, gk, uk, la, lb, grg, nrg, W, warp, r, ldm, rowb, part, rdiag, dmax,
-                                      dmin, amin);
+    int amin = 0;
+    LsqColumns<T, RG, RA, CB, W, 0>::run(A, la, lb, grg, warp, r, rowb, part, rdiag, dmax, dmin, amin);
 
     // R (strict upper part from registers, diagonal = beta) and y to shared memory
 #pragma unroll

@@ -501,21 +501,16 @@ static int launch_lsq_t(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t
   return SAS_OK;
 }
 
-template <typename T, int RG, int RA, int CB, class Asm>
+template <typename T, int RG, int RA, int CB, int W, class Asm>
 static int launch_lsq_mw_t(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t scratch, cudaStream_t st) {
-  const int W = (a.s + RG * RA - 1) / (RG * RA);
-  if (W > 8) {
-    sas_set_error("least-squares multi-warp kernel: s=%d too large for RA=%d", a.s, RA);
-    return SAS_ERR_ARG;
-  }
-  const size_t smem = lsq_mw_smem_bytes<T>(a.s, a.r, W, scratch);
-  auto kern = k_lsq_mw<T, RG, RA, CB, Asm>;
+  const size_t smem = lsq_mw_smem_bytes<T>(a.s, a.r, W, (32 / RG) * CB, scratch);
+  auto kern = k_lsq_mw<T, RG, RA, CB, W, Asm>;
   SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   int occ = 0;
   SAS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * W, smem));
   if (occ < 1) {
-    sas_set_error("least-squares multi-warp kernel does not fit (s=%d r=%d smem=%zu)", a.s, a.r, smem);
+    sas_set_error("least-squares kernel does not fit (s=%d r=%d smem=%zu)", a.s, a.r, smem);
     return SAS_ERR_ARG;
   }
   int64_t grid = (int64_t)occ * pl->sms;
@@ -538,28 +533,32 @@ static bool lsq_force_cta() {
   return v == 1;
 }
 
-// Kernel choice for the batched least squares: k_lsq_mw with W warps per
-// parameter value and an (RG row groups x 32/RG column groups) lane layout
-// holding RA x CB register slots per lane; W = ceil(s / (RG*RA)) <= 8.  Small
-// problems run one warp per parameter value (W = 1).  k_lsq (CTA per p,
-// shared-memory Gram partials) is the fallback for shapes outside the table;
-// SAS_LSQ_KERNEL=cta forces it (A/B checks).
+// Kernel choice for the batched least squares: k_lsq_mw<RG, RA, CB, W> holds
+// [M_w | t_w] in registers, W warps per parameter value, an (RG row groups x
+// 32/RG column groups) lane layout and RA x CB slots per lane, so it covers
+// s <= W*RG*RA rows and r+1 <= (32/RG)*CB columns.  The table is ordered by
+// cost; the first shape that fits wins (configs 1,2: W=1; config 4 (complex
+// 120x9): W=2; config 3 (160x41): W=6; config 5 (200x51): W=8).  k_lsq (CTA
+// per p, shared-memory partials) is the fallback; SAS_LSQ_KERNEL=cta forces it.
 template <typename T, class Asm>
 static int launch_lsq(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t scratch, cudaStream_t st) {
   const int cols = a.r + 1, s = a.s;
-  constexpr bool real = std::is_same<T, double>::value;
   if (!lsq_force_cta()) {
-    if (real) {
-      if (cols <= 12 && s <= 24) return launch_lsq_mw_t<T, 8, 3, 3>(pl, a, as, scratch, st);
-      if (cols <= 12 && s <= 640) return launch_lsq_mw_t<T, 8, 10, 3>(pl, a, as, scratch, st);
-      if (cols <= 24 && s <= 640) return launch_lsq_mw_t<T, 8, 10, 6>(pl, a, as, scratch, st);
-      if (cols <= 32 && s <= 256) return launch_lsq_mw_t<T, 4, 8, 4>(pl, a, as, scratch, st);
-      if (cols <= 48 && s <= 256) return launch_lsq_mw_t<T, 4, 8, 6>(pl, a, as, scratch, st);
-      if (cols <= 64 && s <= 256) return launch_lsq_mw_t<T, 4, 8, 8>(pl, a, as, scratch, st);
+    if constexpr (std::is_same<T, double>::value) {
+      if (cols <= 12 && s <= 24) return launch_lsq_mw_t<T, 8, 3, 3, 1>(pl, a, as, scratch, st);
+      if (cols <= 12 && s <= 80) return launch_lsq_mw_t<T, 8, 10, 3, 1>(pl, a, as, scratch, st);
+      if (cols <= 24 && s <= 80) return launch_lsq_mw_t<T, 8, 10, 6, 1>(pl, a, as, scratch, st);
+      if (cols <= 12 && s <= 256) return launch_lsq_mw_t<T, 8, 8, 3, 4>(pl, a, as, scratch, st);
+      if (cols <= 24 && s <= 256) return launch_lsq_mw_t<T, 8, 8, 6, 4>(pl, a, as, scratch, st);
+      if (cols <= 32 && s <= 128) return launch_lsq_mw_t<T, 4, 8, 4, 4>(pl, a, as, scratch, st);
+      if (cols <= 48 && s <= 168) return launch_lsq_mw_t<T, 4, 7, 6, 6>(pl, a, as, scratch, st);
+      if (cols <= 64 && s <= 224) return launch_lsq_mw_t<T, 4, 7, 8, 8>(pl, a, as, scratch, st);
+      if (cols <= 64 && s <= 256) return launch_lsq_mw_t<T, 4, 8, 8, 8>(pl, a, as, scratch, st);
     } else {
-      if (cols <= 12 && s <= 24) return launch_lsq_mw_t<T, 8, 3, 3>(pl, a, as, scratch, st);
-      if (cols <= 12 && s <= 512) return launch_lsq_mw_t<T, 8, 8, 3>(pl, a, as, scratch, st);
-      if (cols <= 32 && s <= 256) return launch_lsq_mw_t<T, 4, 8, 4>(pl, a, as, scratch, st);
+      if (cols <= 12 && s <= 24) return launch_lsq_mw_t<T, 8, 3, 3, 1>(pl, a, as, scratch, st);
+      if (cols <= 12 && s <= 128) return launch_lsq_mw_t<T, 8, 8, 3, 2>(pl, a, as, scratch, st);
+      if (cols <= 12 && s <= 256) return launch_lsq_mw_t<T, 8, 8, 3, 4>(pl, a, as, scratch, st);
+      if (cols <= 32 && s <= 128) return launch_lsq_mw_t<T, 4, 8, 4, 4>(pl, a, as, scratch, st);
     }
   }
   if (cols <= 32) {
