@@ -179,6 +179,7 @@ struct AsmAffine {
 // as the reference's dense rows_dense(...) @ basis does (online.py:62):
 //   G[i][q] = X[node_q], gmap[i][q] = 0 (diagonal) | 1+e (edge e) | -1 (pad).
 struct AsmStencil {
+  static constexpr int kMaxEdges = 7;  // E + 1 <= 8 gathered rows per selected row
   int E, dp;
   const double* phi;    // s x E x dp
   const double* G;      // s x (E+1) x r
@@ -206,19 +207,40 @@ struct AsmStencil {
       cs[i * E1] = d;
     }
     g.sync();
+    // M = rows @ G: the gathered rows are L2-resident; issue the loads of
+    // kUnroll entries before their FMA chains to keep enough loads in flight.
+    constexpr int kUnroll = 4;
+    const int total = s * r;
     RowMajorWalk wk(g.rank(), g.size(), r);
-    for (int idx = g.rank(); idx < s * r; idx += g.size(), wk.next()) {
-      const int i = wk.i, j = wk.j;
-      const double* gr = G + (int64_t)i * E1 * r + j;
-      const int8_t* mp = gmap + i * E1;
-      double m = 0.0;
-      for (int q = 0; q < E1; ++q) {
-        const int slot = mp[q];
-        if (slot < 0) break;
-        const double a = (slot == 0) ? cs[i * E1] : -cs[i * E1 + slot];
-        m = fma(a, gr[q * r], m);
+    for (int base = g.rank(); base < total; base += kUnroll * g.size()) {
+      double gv[kUnroll][8];
+      int ii[kUnroll], jj[kUnroll];
+#pragma unroll
+      for (int t = 0; t < kUnroll; ++t) {
+        ii[t] = wk.i;
+        jj[t] = wk.j;
+        const bool ok = base + t * g.size() < total;
+        const double* __restrict__ gr = G + ((int64_t)wk.i * E1) * r + wk.j;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) gv[t][q] = (ok && q < E1) ? __ldg(gr + q * r) : 0.0;
+        wk.next();
       }
-      Ms[i * ldm + j] = m;
+#pragma unroll
+      for (int t = 0; t < kUnroll; ++t) {
+        if (base + t * g.size() >= total) break;
+        const int i = ii[t];
+        const int8_t* mp = gmap + i * E1;
+        double m = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (q >= E1) break;
+          const int slot = mp[q];
+          if (slot < 0) break;
+          const double a = (slot == 0) ? cs[i * E1] : -cs[i * E1 + slot];
+          m = fma(a, gv[t][q], m);
+        }
+        Ms[i * ldm + jj[t]] = m;
+      }
     }
   }
 };

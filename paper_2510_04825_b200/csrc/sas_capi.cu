@@ -271,7 +271,7 @@ extern "C" int sas_plan_create(const sas_desc* desc, const void* X, int64_t n, i
       ARG_CHECK(desc->term_kind[k] >= 0 && desc->term_kind[k] <= 3, "affine: bad coefficient kind %d", desc->term_kind[k]);
   } else if (desc->op_kind == SAS_OP_STENCIL) {
     ARG_CHECK(desc->dtype == SAS_F64 && !desc->param_complex, "stencil: real f64 only");
-    ARG_CHECK(desc->n_edges >= 1 && desc->n_edges <= 8, "stencil: 1..8 edges per row");
+    ARG_CHECK(desc->n_edges >= 1 && desc->n_edges <= 7, "stencil: 1..7 edges per row");
     ARG_CHECK(desc->edge_nbr && desc->edge_phi && desc->edge_div > 0, "stencil: edge_nbr, edge_phi, edge_div required");
     for (int64_t q = 0; q < (int64_t)s * desc->n_edges; ++q)
       ARG_CHECK(desc->edge_nbr[q] < n, "stencil: neighbour index out of range");
