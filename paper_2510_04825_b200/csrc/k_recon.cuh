@@ -1,9 +1,73 @@
 // K5/K6: reconstruction x = X c (OnlineSolution.lift, online.py:50-54) and the
-// full-residual checker ||A(p) x - b|| / max(||b||, 1e-300) (cli.py:285, 344-351)
-// evaluated without materialising x: each thread recomputes the x entries of a
-// row's stencil neighbourhood from X and c.
+// full-residual checker ||A(p) x - b|| / max(||b||, 1e-300) (cli.py:285, 344-351).
+//
+// K5 (real): x^T = X C^T as a DMMA GEMM (mma.sync.m8n8k4.f64): A = X tile
+// (64 nodes x r, staged in shared memory), B = C^T tile (r x 64 parameters),
+// one warp per 8 nodes x 64 parameters, K = r padded to 4.  The residual then
+// runs on the materialised x in chunks of parameters (k_resid_*_x).
 #pragma once
 #include "sas_common.cuh"
+
+__device__ __forceinline__ void dmma884_r(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+constexpr int kLiftNodes = 64;  // nodes per CTA (8 warps x 8)
+constexpr int kLiftPar = 64;    // parameter values per CTA (8 n-tiles of 8)
+
+// shared-memory row stride >= 4*ceil(r/4) with stride == 4 (mod 16) doubles, so the
+// 8 x 4 A/B fragments of a half-warp hit distinct banks
+__host__ __device__ inline int lift_ld(int r) {
+  int kp = ((r + 3) / 4) * 4;
+  while (kp % 16 != 4) ++kp;
+  return kp;
+}
+
+// grid = (ceil(n/64), ceil(P/64)); block 256
+__global__ void __launch_bounds__(256) k_lift_dmma(const double* __restrict__ X, int64_t n, int r,
+                                                   const double* __restrict__ C, int64_t P,
+                                                   double* __restrict__ x) {
+  extern __shared__ __align__(16) double lsm[];
+  const int ld = lift_ld(r);
+  const int kp = ((r + 3) / 4) * 4;
+  double* Xs = lsm;                      // 64 x ld
+  double* Cs = lsm + kLiftNodes * ld;    // 64 x ld
+  const int64_t i0 = (int64_t)blockIdx.x * kLiftNodes;
+  const int64_t p0 = (int64_t)blockIdx.y * kLiftPar;
+  for (int e = threadIdx.x; e < kLiftNodes * kp; e += blockDim.x) {
+    const int row = e / kp, k = e - row * kp;
+    const int64_t i = i0 + row, p = p0 + row;
+    Xs[row * ld + k] = (i < n && k < r) ? X[i * r + k] : 0.0;
+    Cs[row * ld + k] = (p < P && k < r) ? C[p * r + k] : 0.0;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double acc[8][2];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) acc[t][0] = acc[t][1] = 0.0;
+  const double* xa = Xs + (warp * 8 + (lane >> 2)) * ld + (lane & 3);
+  const double* cb = Cs + (lane >> 2) * ld + (lane & 3);
+  for (int k0 = 0; k0 < kp; k0 += 4) {
+    const double a = xa[k0];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) dmma884_r(acc[t][0], acc[t][1], a, cb[t * 8 * ld + k0]);
+  }
+  const int64_t i = i0 + warp * 8 + (lane >> 2);
+  if (i < n) {
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int64_t p = p0 + t * 8 + 2 * (lane & 3);
+      if (p < P) x[p * n + i] = acc[t][0];
+      if (p + 1 < P) x[(p + 1) * n + i] = acc[t][1];
+    }
+  }
+}
+
+// Stencil residual on a materialised x (P x n): kResidPB parameter values per
+// blockIdx.y share each node's phi / neighbour reads; partial sums of
+// |Ax - b|^2 and |b|^2 per CTA and parameter (defined below).
 
 constexpr int kLiftPT = 8;  // parameter values per CTA
 
@@ -47,54 +111,6 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   if (threadIdx.x == 0)
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
   return t;  // valid on thread 0
-}
-
-// Stencil residual for ONE parameter value per blockIdx.y; grid.x strides over rows.
-// Partial sums of |A x - b|^2 and |b|^2 per CTA go to part[(p * gridDim.x + bx) * 2].
-// Coefficients c_e(p) = exp(sum_k p_k phi[row][e][k]) / hh as in the online rows.
-__global__ void __launch_bounds__(256) k_resid_stencil(const double* __restrict__ X, int64_t n, int r,
-                                                       const int64_t* __restrict__ nbr,   // n x E
-                                                       const double* __restrict__ phi,    // n x E x dp
-                                                       int E, int dp, double hh,
-                                                       const double* __restrict__ b,      // n
-                                                       const double* __restrict__ params, // P x dp
-                                                       const double* __restrict__ coef,   // P x r
-                                                       double* __restrict__ part) {
-  __shared__ double cs[64];
-  __shared__ double red[32];
-  const int64_t p = blockIdx.y;
-  for (int j = threadIdx.x; j < r; j += blockDim.x) cs[j] = coef[p * r + j];
-  __syncthreads();
-  const double* pp = params + p * dp;
-  double rr = 0.0, bb = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double xi = 0.0;
-    for (int j = 0; j < r; ++j) xi = fma(X[i * r + j], cs[j], xi);
-    double diag = 0.0, off = 0.0;
-    for (int e = 0; e < E; ++e) {
-      const double* ph = phi + (i * E + e) * dp;
-      double arg = dmul_exact(pp[0], ph[0]);
-      for (int k = 1; k < dp; ++k) arg = dadd_exact(arg, dmul_exact(pp[k], ph[k]));
-      const double c = exp(arg) / hh;
-      diag = dadd_exact(diag, c);
-      const int64_t m = nbr[i * E + e];
-      if (m >= 0) {
-        double xm = 0.0;
-        for (int j = 0; j < r; ++j) xm = fma(X[m * r + j], cs[j], xm);
-        off = fma(-c, xm, off);
-      }
-    }
-    const double ax = fma(diag, xi, off);
-    const double res = ax - b[i];
-    rr = fma(res, res, rr);
-    bb = fma(b[i], b[i], bb);
-  }
-  double trr = block_sum(rr, red);
-  double tbb = block_sum(bb, red);
-  if (threadIdx.x == 0) {
-    part[(p * gridDim.x + blockIdx.x) * 2] = trr;
-    part[(p * gridDim.x + blockIdx.x) * 2 + 1] = tbb;
-  }
 }
 
 // Affine residual: sum_k f_k(p) A_k x - b with CSR A_k, for one p per blockIdx.y.
@@ -188,4 +204,64 @@ __global__ void k_resid_finish(const double* __restrict__ part, int nb, int64_t 
     bb += part[(p * nb + q) * 2 + 1];
   }
   relres[p] = sqrt(rr) / fmax(sqrt(bb), 1e-300);
+}
+
+constexpr int kResidPB = 8;  // parameter values per thread pass (amortises the phi / nbr reads)
+
+// grid = (nb, ceil(P / kResidPB)); x is P x n (this chunk), params P x dp
+__global__ void __launch_bounds__(256) k_resid_stencil_x(const double* __restrict__ x, int64_t n, int64_t P,
+                                                         const int64_t* __restrict__ nbr,
+                                                         const double* __restrict__ phi, int E, int dp, double hh,
+                                                         const double* __restrict__ b,
+                                                         const double* __restrict__ params,
+                                                         double* __restrict__ part) {
+  __shared__ double red[32];
+  __shared__ double ps[kResidPB * 8];
+  const int64_t pb = (int64_t)blockIdx.y * kResidPB;
+  const int npb = (int)((P - pb) < kResidPB ? (P - pb) : kResidPB);
+  for (int e = threadIdx.x; e < kResidPB * dp; e += blockDim.x) {
+    const int u = e / dp;
+    ps[e] = (u < npb) ? params[(pb + u) * dp + (e - u * dp)] : 0.0;
+  }
+  __syncthreads();
+  double rr[kResidPB];
+#pragma unroll
+  for (int u = 0; u < kResidPB; ++u) rr[u] = 0.0;
+  double bb = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double diag[kResidPB], off[kResidPB];
+#pragma unroll
+    for (int u = 0; u < kResidPB; ++u) diag[u] = off[u] = 0.0;
+    for (int e = 0; e < E; ++e) {
+      const double* ph = phi + (i * E + e) * dp;
+      double phv[8];
+      for (int k = 0; k < dp; ++k) phv[k] = __ldg(ph + k);
+      const int64_t m = __ldg(nbr + i * E + e);
+#pragma unroll
+      for (int u = 0; u < kResidPB; ++u) {
+        if (u >= npb) break;
+        double arg = dmul_exact(ps[u * dp], phv[0]);
+        for (int k = 1; k < dp; ++k) arg = dadd_exact(arg, dmul_exact(ps[u * dp + k], phv[k]));
+        const double c = exp(arg) / hh;
+        diag[u] = dadd_exact(diag[u], c);
+        if (m >= 0) off[u] = fma(-c, __ldg(x + (pb + u) * n + m), off[u]);
+      }
+    }
+    const double bi = b[i];
+#pragma unroll
+    for (int u = 0; u < kResidPB; ++u) {
+      if (u >= npb) break;
+      const double res = fma(diag[u], x[(pb + u) * n + i], off[u]) - bi;
+      rr[u] = fma(res, res, rr[u]);
+    }
+    bb = fma(bi, bi, bb);
+  }
+  const double tbb = block_sum(bb, red);
+  for (int u = 0; u < npb; ++u) {
+    const double trr = block_sum(rr[u], red);
+    if (threadIdx.x == 0) {
+      part[((pb + u) * gridDim.x + blockIdx.x) * 2] = trr;
+      part[((pb + u) * gridDim.x + blockIdx.x) * 2 + 1] = tbb;
+    }
+  }
 }

@@ -132,6 +132,8 @@ struct sas_plan {
   int64_t Mscr_P = 0;
   double* rpart = nullptr;
   int64_t rpart_n = 0;
+  double* xscr = nullptr;   // materialised x chunk for the residual checker
+  int64_t xscr_n = 0;
   void* fco = nullptr;
   int64_t fco_n = 0;
   // host-call staging
@@ -202,7 +204,7 @@ static void plan_free(sas_plan* pl) {
   DevGuard g(pl->device);
   void* ptrs[] = {pl->X, pl->S, pl->w, pl->t, pl->proj, pl->kind, pl->scale, pl->rate, pl->blocks,
                   pl->phi, pl->G, pl->gmap, pl->pts, pl->D, pl->Dfrag, pl->Xfrag, pl->full_nbr, pl->full_phi, pl->full_b,
-                  pl->csr_rp_d, pl->csr_ci_d, pl->csr_va_d, pl->Mscr, pl->rpart, pl->fco,
+                  pl->csr_rp_d, pl->csr_ci_d, pl->csr_va_d, pl->Mscr, pl->rpart, pl->xscr, pl->fco,
                   pl->h_params, pl->h_ctab, pl->h_rhs, pl->h_coef, pl->h_sres, pl->h_outv,
                   pl->h_status, pl->h_bad};
   for (void* p : ptrs)
@@ -272,6 +274,7 @@ extern "C" int sas_plan_create(const sas_desc* desc, const void* X, int64_t n, i
   } else if (desc->op_kind == SAS_OP_STENCIL) {
     ARG_CHECK(desc->dtype == SAS_F64 && !desc->param_complex, "stencil: real f64 only");
     ARG_CHECK(desc->n_edges >= 1 && desc->n_edges <= 7, "stencil: 1..7 edges per row");
+    ARG_CHECK(desc->param_dim <= 8, "stencil: at most 8 coefficient parameters");
     ARG_CHECK(desc->edge_nbr && desc->edge_phi && desc->edge_div > 0, "stencil: edge_nbr, edge_phi, edge_div required");
     for (int64_t q = 0; q < (int64_t)s * desc->n_edges; ++q)
       ARG_CHECK(desc->edge_nbr[q] < n, "stencil: neighbour index out of range");
@@ -760,6 +763,18 @@ extern "C" int sas_solve_host(sas_plan* pl, const void* params, int64_t P, const
   return SAS_OK;
 }
 
+static int launch_lift_dmma(sas_plan* pl, const double* coef, int64_t P, double* x, cudaStream_t st) {
+  const size_t smem = 2 * (size_t)kLiftNodes * lift_ld(pl->r) * sizeof(double);
+  SAS_CUDA_CHECK(cudaFuncSetAttribute(k_lift_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  for (int64_t p0 = 0; p0 < P; p0 += 65535LL * kLiftPar) {
+    const int64_t pc = (P - p0 < 65535LL * kLiftPar) ? P - p0 : 65535LL * kLiftPar;
+    dim3 grid((unsigned)((pl->n + kLiftNodes - 1) / kLiftNodes), (unsigned)((pc + kLiftPar - 1) / kLiftPar));
+    k_lift_dmma<<<grid, 256, smem, st>>>((const double*)pl->X, pl->n, pl->r, coef + p0 * pl->r, pc, x + p0 * pl->n);
+  }
+  SAS_CUDA_CHECK(cudaGetLastError());
+  return SAS_OK;
+}
+
 extern "C" int sas_lift(sas_plan* pl, const void* coef, int64_t P, void* x, void* stream) {
   ARG_CHECK(pl, "null plan");
   if (P == 0) return SAS_OK;
@@ -767,11 +782,14 @@ extern "C" int sas_lift(sas_plan* pl, const void* coef, int64_t P, void* x, void
   DevGuard g(pl->device);
   cudaStream_t st = (cudaStream_t)stream;
   dim3 grid((unsigned)((pl->n + 255) / 256), (unsigned)((P + kLiftPT - 1) / kLiftPT));
-  ARG_CHECK(grid.y <= 65535, "sas_lift: P too large for one call (max %d)", 65535 * kLiftPT);
-  if (pl->dtype == SAS_C128)
+  ARG_CHECK(pl->dtype != SAS_C128 || grid.y <= 65535, "sas_lift: P too large for one call (max %d)",
+            65535 * kLiftPT);
+  if (pl->dtype == SAS_C128) {
     k_lift<cplx><<<grid, 256, 0, st>>>((const cplx*)pl->X, pl->n, pl->r, (const cplx*)coef, P, (cplx*)x);
-  else
-    k_lift<double><<<grid, 256, 0, st>>>((const double*)pl->X, pl->n, pl->r, (const double*)coef, P, (double*)x);
+  } else {
+    int rc = launch_lift_dmma(pl, (const double*)coef, P, (double*)x, st);
+    if (rc) return rc;
+  }
   SAS_CUDA_CHECK(cudaGetLastError());
   pl->last_launches = 1;
   return SAS_OK;
@@ -846,11 +864,21 @@ extern "C" int sas_residual(sas_plan* pl, const void* params, const void* coef, 
   pl->last_launches = 0;
   dim3 grid(nb, (unsigned)P);
   if (pl->op == SAS_OP_STENCIL) {
+    // x for a chunk of parameters (K5, DMMA), then the stencil residual on it (K6);
+    // the chunk keeps the x scratch within ~2 GB
     ARG_CHECK(pl->full_nbr, "sas_residual: stencil operator not set");
-    k_resid_stencil<<<grid, 256, 0, st>>>((const double*)pl->X, pl->n, pl->r, pl->full_nbr, pl->full_phi, pl->E,
-                                          pl->dp, pl->hh, (const double*)pl->full_b, (const double*)params,
-                                          (const double*)coef, pl->rpart);
-    pl->last_launches++;
+    int64_t chunk = (2ll << 30) / (pl->n * (int64_t)sizeof(double));
+    chunk = chunk < 1 ? 1 : (chunk > P ? P : chunk);
+    if ((rc = ensure(&pl->xscr, &pl->xscr_n, chunk * pl->n * (int64_t)sizeof(double)))) return rc;
+    for (int64_t p0 = 0; p0 < P; p0 += chunk) {
+      const int64_t pc = (P - p0 < chunk) ? P - p0 : chunk;
+      if ((rc = launch_lift_dmma(pl, (const double*)coef + p0 * pl->r, pc, pl->xscr, st))) return rc;
+      dim3 g2(nb, (unsigned)((pc + kResidPB - 1) / kResidPB));
+      k_resid_stencil_x<<<g2, 256, 0, st>>>(pl->xscr, pl->n, pc, pl->full_nbr, pl->full_phi, pl->E, pl->dp, pl->hh,
+                                            (const double*)pl->full_b, (const double*)params + p0 * pl->dp,
+                                            pl->rpart + p0 * nb * 2);
+      pl->last_launches += 2;
+    }
   } else if (pl->op == SAS_OP_AFFINE) {
     ARG_CHECK(!pl->csr_rp.empty(), "sas_residual: affine operator not set");
     for (int k = 0; k < pl->K; ++k)
@@ -878,8 +906,7 @@ extern "C" int sas_residual(sas_plan* pl, const void* params, const void* coef, 
     // Gaussian kernel: lift x first (P x n scratch), then re-evaluate kernel rows.
     double* xs = nullptr;
     if ((rc = dalloc(&xs, (size_t)P * pl->n * sizeof(double)))) return rc;
-    dim3 lg((unsigned)((pl->n + 255) / 256), (unsigned)((P + kLiftPT - 1) / kLiftPT));
-    k_lift<double><<<lg, 256, 0, st>>>((const double*)pl->X, pl->n, pl->r, (const double*)coef, P, xs);
+    if ((rc = launch_lift_dmma(pl, (const double*)coef, P, xs, st))) { cudaFree(xs); return rc; }
     k_resid_gauss<<<grid, 256, 0, st>>>((const double*)pl->X, pl->n, pl->r, pl->pts, pl->pdim, pl->ridge,
                                         (const double*)pl->full_b, (const double*)params, xs, pl->rpart);
     cudaError_t e = cudaStreamSynchronize(st);

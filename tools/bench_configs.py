@@ -75,7 +75,7 @@ def oracle_coef(prob, basis, sel, p):
     return c, sres, floor
 
 
-def run(cfg, steps, dev, synthetic=False, P=None, check=True):
+def run(cfg, steps, dev, synthetic=False, P=None, check=True, resid_count=0):
     t0 = time.perf_counter()
     prob = problems.build(cfg)
     if synthetic and cfg != 2:
@@ -127,7 +127,26 @@ def run(cfg, steps, dev, synthetic=False, P=None, check=True):
         d = float(np.linalg.norm(coef[k] - c) / np.linalg.norm(c))
         checks.append({"k": int(k), "rel_diff": d, "floor": float(floor)})
         worst = max(worst, d / max(1e-10, 10 * floor))
+    resid = None
+    if resid_count:
+        sub = params[:resid_count]
+        online.set_full_operator(plan)
+        online.relative_residual(plan, sub[:2], coef[:2])  # warm-up
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        rr = online.relative_residual(plan, sub, coef[:resid_count])
+        torch.cuda.synchronize()
+        t_rr = time.perf_counter() - t1
+        resid = {"count": resid_count, "seconds": round(t_rr, 4), "median_relres": float(np.median(rr))}
+        if prob.system.n <= 2_000_000:
+            x = basis.basis @ coef[0]
+            a = prob.system.matrix(params[0])
+            b = prob.system.full_rhs(params[0])
+            ref = online_ref.relative_residual(a, x, b)
+            resid["relres0_gpu"] = float(rr[0])
+            resid["relres0_oracle"] = ref
     return {
+        "resid": resid,
         "config": cfg, "name": prob.key, "n": prob.system.n, "r": basis.rank, "s": sel.size, "P": P,
         "dtype": "c128" if g.complex else "f64", "basis": src, "offline_s": round(t_off, 1),
         "ms_per_sweep": round(ms, 3), "p_per_s": round(P / ms * 1e3, 1),
@@ -145,10 +164,12 @@ def main():
     ap.add_argument("--synthetic", action="store_true", help="seeded orthonormal basis for every config but 2")
     ap.add_argument("--P", type=int, default=None)
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--resid", type=int, default=0, help="time the full-residual checker on the first N p")
     args = ap.parse_args()
     dev = torch.device("cuda:0")
     for cfg in [int(c) for c in args.configs.split(",")]:
-        res = run(cfg, args.steps, dev, synthetic=args.synthetic, P=args.P, check=not args.no_parity)
+        res = run(cfg, args.steps, dev, synthetic=args.synthetic, P=args.P, check=not args.no_parity,
+                  resid_count=args.resid)
         line = json.dumps(res)
         print(line, flush=True)
         if args.out:
