@@ -763,13 +763,20 @@ extern "C" int sas_solve_host(sas_plan* pl, const void* params, int64_t P, const
   return SAS_OK;
 }
 
-static int launch_lift_dmma(sas_plan* pl, const double* coef, int64_t P, double* x, cudaStream_t st) {
+// x = X c for P parameters: P x n (node_major = false) or n x ldx (node_major = true)
+static int launch_lift_dmma(sas_plan* pl, const double* coef, int64_t P, double* x, cudaStream_t st,
+                            bool node_major = false, int64_t ldx = 0) {
   const size_t smem = 2 * (size_t)kLiftNodes * lift_ld(pl->r) * sizeof(double);
-  SAS_CUDA_CHECK(cudaFuncSetAttribute(k_lift_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SAS_CUDA_CHECK(cudaFuncSetAttribute(k_lift_dmma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SAS_CUDA_CHECK(cudaFuncSetAttribute(k_lift_dmma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   for (int64_t p0 = 0; p0 < P; p0 += 65535LL * kLiftPar) {
     const int64_t pc = (P - p0 < 65535LL * kLiftPar) ? P - p0 : 65535LL * kLiftPar;
     dim3 grid((unsigned)((pl->n + kLiftNodes - 1) / kLiftNodes), (unsigned)((pc + kLiftPar - 1) / kLiftPar));
-    k_lift_dmma<<<grid, 256, smem, st>>>((const double*)pl->X, pl->n, pl->r, coef + p0 * pl->r, pc, x + p0 * pl->n);
+    if (node_major)
+      k_lift_dmma<true><<<grid, 256, smem, st>>>((const double*)pl->X, pl->n, pl->r, coef + p0 * pl->r, pc, x + p0, ldx);
+    else
+      k_lift_dmma<false><<<grid, 256, smem, st>>>((const double*)pl->X, pl->n, pl->r, coef + p0 * pl->r, pc,
+                                                  x + p0 * pl->n, 0);
   }
   SAS_CUDA_CHECK(cudaGetLastError());
   return SAS_OK;
@@ -872,9 +879,9 @@ extern "C" int sas_residual(sas_plan* pl, const void* params, const void* coef, 
     if ((rc = ensure(&pl->xscr, &pl->xscr_n, chunk * pl->n * (int64_t)sizeof(double)))) return rc;
     for (int64_t p0 = 0; p0 < P; p0 += chunk) {
       const int64_t pc = (P - p0 < chunk) ? P - p0 : chunk;
-      if ((rc = launch_lift_dmma(pl, (const double*)coef + p0 * pl->r, pc, pl->xscr, st))) return rc;
+      if ((rc = launch_lift_dmma(pl, (const double*)coef + p0 * pl->r, pc, pl->xscr, st, true, pc))) return rc;
       dim3 g2(nb, (unsigned)((pc + kResidPB - 1) / kResidPB));
-      k_resid_stencil_x<<<g2, 256, 0, st>>>(pl->xscr, pl->n, pc, pl->full_nbr, pl->full_phi, pl->E, pl->dp, pl->hh,
+      k_resid_stencil_x<<<g2, 256, 0, st>>>(pl->xscr, pl->n, pc, pc, pl->full_nbr, pl->full_phi, pl->E, pl->dp, pl->hh,
                                             (const double*)pl->full_b, (const double*)params + p0 * pl->dp,
                                             pl->rpart + p0 * nb * 2);
       pl->last_launches += 2;
