@@ -200,17 +200,25 @@ def main():
     from paper_2510_04825_b200 import parallel
     env = parallel.dist_env()
     import torch
+    # SAS_BENCH_SHARED_GPU=1: test hook for the N>1 code path on a single-GPU box
+    # (all ranks on cuda:0, host collectives over gloo; ranks never wait on each
+    # other inside a kernel).  Production runs use one GPU per rank and NCCL.
+    shared = os.environ.get("SAS_BENCH_SHARED_GPU") == "1"
+    gpu = 0 if shared else env.local_rank
     if env.world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(env.local_rank)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{env.local_rank}"))
+        torch.cuda.set_device(gpu)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{gpu}"))
     P = args.P or P_PER_GPU[args.config]
     K, W = args.steps, args.warmup
 
     if args.impl == "reference":
         return run_reference_arm(args, env, P)
 
-    dev = torch.device(f"cuda:{env.local_rank}")
+    dev = torch.device(f"cuda:{gpu}")
     torch.cuda.set_device(dev)
     from paper_2510_04825_b200 import online
     prob, basis, sel, t_off = build_inputs(args.config, env, dev)
@@ -222,7 +230,7 @@ def main():
     Pl = len(my_params)
 
     t0 = time.perf_counter()
-    plan = online.precompute_online(sysm, basis, sel, device=env.local_rank)
+    plan = online.precompute_online(sysm, basis, sel, device=gpu)
     t_plan = time.perf_counter() - t0
     g = plan.gpu
     params_t = online.device_params(plan, my_params, device=dev)

@@ -62,10 +62,15 @@ def broadcast_inputs(arrays: dict, src: int = 0, local_rank: int = 0) -> dict:
     import torch.distributed as dist
     backend = dist.get_backend()
     dev = _device_for(backend, local_rank)
-    meta = [{k: (v.shape, str(v.dtype)) for k, v in arrays.items()} if dist.get_rank() == src else None]
+    meta = [{k: (None if v is None else (np.asarray(v).shape, str(np.asarray(v).dtype)))
+             for k, v in arrays.items()} if dist.get_rank() == src else None]
     dist.broadcast_object_list(meta, src=src)
     out = {}
-    for key, (shape, dtype) in sorted(meta[0].items()):
+    for key, spec in sorted(meta[0].items()):
+        if spec is None:  # e.g. an unweighted selector
+            out[key] = None
+            continue
+        shape, dtype = spec
         npdt = np.dtype(dtype)
         if dist.get_rank() == src:
             a = np.ascontiguousarray(arrays[key])

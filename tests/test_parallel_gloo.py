@@ -28,8 +28,9 @@ def _worker(rank, world, port, out):
     env = parallel.dist_env()
     rng = np.random.default_rng(0)
     arrays = {"X": rng.standard_normal((50, 7)), "S": np.arange(10, dtype=np.int64) * 3,
-              "w": rng.uniform(0.5, 2, 10)} if env.rank == 0 else {}
+              "w": rng.uniform(0.5, 2, 10), "none": None} if env.rank == 0 else {}
     got = parallel.broadcast_inputs(arrays, src=0)
+    assert got["none"] is None
     ref = {"X": np.random.default_rng(0).standard_normal((50, 7))}
     ok_bcast = np.array_equal(got["X"], ref["X"]) and np.array_equal(got["S"], np.arange(10) * 3)
     P = 23
