@@ -66,7 +66,7 @@ __host__ __device__ inline void gauss_row_blocks(int s, int* gy, int* rows_cta) 
 // Plan-time layouts put every DMMA fragment a warp needs for one k-step in 32
 // consecutive doubles (lane order), so a pipeline stage is two contiguous
 // blocks (the CTA's D fragments and the X^T fragments of one K chunk):
-//   Dfrag[rb][ch][g][ks][lane] = D[rb*rows_cta + 8g + lane/4][ch*KC + 4ks + lane%4]
+//   Dfrag[rb][ch][g][ks][lane] = D[rb*rows_cta + 8g + lane/4][ch*KC + 4ks + lane%4] * 2048/ln2
 //   Xfrag[ch][t][ks][lane]     = X[ch*KC + 4ks + lane%4][8t + lane/4]
 // One thread issues cp.async.bulk (SASS UBLKCP) per stage with an mbarrier
 // transaction count; warps wait on the stage's full barrier and release it
@@ -90,7 +90,8 @@ __global__ void k_gauss_pack_dfrag(const double* __restrict__ D, int64_t ldd, in
   int rb = (int)(rest / nchunks);
   int row = rb * rows_cta + 8 * g + (lane >> 2);
   int64_t l = ch * kGaussKC + 4 * ks + (lane & 3);
-  Df[idx] = (row < s && l < n) ? D[(int64_t)row * ldd + l] : 0.0;
+  // pre-scaled by 2048/ln2: the exponential takes its argument in table units
+  Df[idx] = (row < s && l < n) ? D[(int64_t)row * ldd + l] * SAS_INVLN2X2K : 0.0;
 }
 
 __global__ void k_gauss_pack_xfrag(const double* __restrict__ X, int64_t n, int r, int nt, int64_t nchunks,
@@ -216,7 +217,7 @@ k_gauss_rows3(const double* __restrict__ Df, const double* __restrict__ Xf, cons
       const bool diag = (4 * ks + (lane & 3)) == dcol;
 #pragma unroll
       for (int u = 0; u < PW; ++u) {
-        const double e = sas_exp64_t2k_ridge(dv * ninv[u], tab_s, diag, onepr);
+        const double e = sas_exp64_t2k_ridge(dv, ninv[u], tab_s, diag, onepr);
 #pragma unroll
         for (int t = 0; t < NT; ++t) dmma884(acc[u][t][0], acc[u][t][1], e, bf[t]);
       }

@@ -63,21 +63,21 @@ void sas_set_error(const char* fmt, ...) {
     }                               \
   } while (0)
 
-// Host mirror of sas_exp64_t2k (the K3 exponential), bit for bit.
+// Host mirror of the K3 exponential (sas_exp64_t2k_ridge(x, 2048/ln2)), bit for bit.
 double sas_exp64_host(double x) {
-  volatile double kd = fma(x, SAS_INVLN2X2K, SAS_EXP_MAGIC);
-  double kdv = kd;
+  const double kd = fma(x, SAS_INVLN2X2K, SAS_EXP_MAGIC);
   int64_t bits;
-  memcpy(&bits, &kdv, 8);
+  memcpy(&bits, &kd, 8);
   const int ki = (int)(uint32_t)(bits & 0xffffffffu);
-  const double kf = kdv - SAS_EXP_MAGIC;
-  double r = fma(-kf, SAS_LN2D2K_HI, x);
-  r = fma(-kf, SAS_LN2D2K_LO, r);
-  double q = fma(r, 1.0 / 6.0, 0.5);
-  q = fma(q, r, 1.0);
-  q = q * r;
-  const double t = h_exp2_tab2048[ki & 2047];
-  double res = fma(t, q, t);
+  volatile double kfv = kd - SAS_EXP_MAGIC;
+  const double kf = kfv;
+  const double r = fma(x, SAS_INVLN2X2K, -kf);
+  double q = fma(r, SAS_EXP2K_A3, SAS_EXP2K_A2);
+  q = fma(q, r, SAS_EXP2K_A1);
+  volatile double qv = q * r;
+  q = qv;
+  const double tab = h_exp2_tab2048[ki & 2047];
+  double res = fma(tab, q, tab);
   int64_t rb;
   memcpy(&rb, &res, 8);
   rb += (int64_t)(ki >> 11) << 52;
@@ -240,10 +240,10 @@ __global__ void k_debug_exp64(const double* x, double* y, int64_t n) {
   for (int j = threadIdx.x; j < 2048; j += blockDim.x) tab_s[j] = g_exp2_tab2048[j];
   __syncthreads();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    y[i] = sas_exp64_t2k(x[i], tab_s);
+    y[i] = sas_exp64_t2k_ridge(x[i], SAS_INVLN2X2K, tab_s, false, 0.0);
 }
 
-// Device evaluation of the kernel-row exp (sas_exp64) for accuracy tests; device pointers.
+// Device evaluation of the K3 exponential (on t = x * 2048/ln2) for accuracy tests; device pointers.
 extern "C" int sas_debug_exp64(const double* x, double* y, int64_t n, void* stream) {
   if (n <= 0) return SAS_OK;
   k_debug_exp64<<<256, 256, 0, (cudaStream_t)stream>>>(x, y, n);

@@ -254,22 +254,32 @@ __device__ __forceinline__ double sas_exp64_t2k(double x, const double* __restri
   return __hiloint2double(hi & keep, __double2loint(res) & keep);
 }
 
-// sas_exp64_t2k with the kernel-row ridge folded in: on the diagonal entry
-// (l == S_i) D = 0 exactly, so x = -0, r = +-0, q = +-0 and the result is the
-// table value; selecting (1 + ridge) instead of 2^0 gives exactly the
-// reference's exp(-0) + lam without an FP64 add.
-__device__ __forceinline__ double sas_exp64_t2k_ridge(double x, const double* __restrict__ tab_s, bool diag,
-                                                      double onepr) {
-  const double kd = fma(x, SAS_INVLN2X2K, SAS_EXP_MAGIC);
+// K3 exponential in "table units": e^(a*b) for a = D' (kernel-row distance
+// pre-scaled by 2048/ln2 at plan time) and b = -inv = -1/(2p^2), i.e. the
+// argument a*b is x * 2048/ln2.  k = rint(a*b) and r = a*b - k both come from
+// one FMA on the exact product (|r| <= 1/2, one rounding), so no rounded copy
+// of the argument is formed; e^x = 2^(k/2048) 2^(r/2048), 2^(r/2048) - 1 =
+// r (a1 + r (a2 + r a3)) with a_i = (ln2/2048)^i / i! (truncation <= 3.5e-17).
+// 7 FP64-pipe ops.  The plan-time rounding of D' gives a relative error
+// ~|x| eps/2, the same as the rounding of x = -D*inv in the reference.  The kernel-row
+// ridge is folded in: on the diagonal entry (l == S_i) D = 0, so r = +-0,
+// q = +-0 and the result is the selected table value; selecting (1 + ridge)
+// gives exactly the reference's exp(-0) + lam.
+#define SAS_EXP2K_A1 0x1.62e42fefa39efp-12
+#define SAS_EXP2K_A2 0x1.ebfbdff82c58fp-25
+#define SAS_EXP2K_A3 0x1.c6b08d704a0c0p-38
+
+__device__ __forceinline__ double sas_exp64_t2k_ridge(double a, double b, const double* __restrict__ tab_s,
+                                                      bool diag, double onepr) {
+  const double kd = fma(a, b, SAS_EXP_MAGIC);
   const int ki = __double2loint(kd);
-  const double kf = kd - SAS_EXP_MAGIC;
-  double r = fma(-kf, SAS_LN2D2K_HI, x);
-  r = fma(-kf, SAS_LN2D2K_LO, r);
-  double q = fma(r, 1.0 / 6.0, 0.5);
-  q = fma(q, r, 1.0);
+  const double kf = __dsub_rn(kd, SAS_EXP_MAGIC);
+  const double r = fma(a, b, -kf);
+  double q = fma(r, SAS_EXP2K_A3, SAS_EXP2K_A2);
+  q = fma(q, r, SAS_EXP2K_A1);
   q = q * r;
-  const double t = diag ? onepr : tab_s[ki & 2047];
-  const double res = fma(t, q, t);
+  const double tv = diag ? onepr : tab_s[ki & 2047];
+  const double res = fma(tv, q, tv);
   const int hi = __double2hiint(res) + ((ki >> 11) << 20);
   const int keep = (ki >= SAS_EXP2K_KMIN) ? -1 : 0;
   return __hiloint2double(hi & keep, __double2loint(res) & keep);
