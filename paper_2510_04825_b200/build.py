@@ -41,7 +41,8 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and up_to_date():
         return LIB
-    cmd = [nvcc_path(), "-std=c++17", "-O3", "-lineinfo", *ARCH, "-shared", "-Xcompiler", "-fPIC",
+    extra = os.environ.get("SAS_NVCC_FLAGS", "").split()
+    cmd = [nvcc_path(), "-std=c++17", "-O3", "-lineinfo", *ARCH, *extra, "-shared", "-Xcompiler", "-fPIC",
            "-Xptxas", "-v" if verbose else "-O3", "-o", str(LIB) + ".tmp", str(CSRC / "sas_capi.cu")]
     res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
     if res.returncode != 0:

@@ -73,6 +73,10 @@ __host__ __device__ inline void gauss_row_blocks(int s, int* gy, int* rows_cta) 
 // through an empty barrier, so there is no CTA-wide __syncthreads in the loop
 // and fragment reads are conflict-free (lane-contiguous 8-byte loads).
 // ===========================================================================
+#ifndef K3_UNROLL
+#define K3_UNROLL 2
+#endif
+constexpr int kK3Unroll = K3_UNROLL;  // k-steps unrolled per loop iteration
 constexpr int kG3Stages = 3;
 constexpr int kG3KS = kGaussKC / 4;  // k-steps per chunk
 
@@ -208,7 +212,7 @@ k_gauss_rows3(const double* __restrict__ Df, const double* __restrict__ Xf, cons
     const double* xsb = gsm + (size_t)b * stage_d + nrg * kG3KS * 32 + lane;
     const int64_t l0 = ch * kGaussKC;
     const int dcol = (srow >= l0 && srow < l0 + kGaussKC) ? (int)(srow - l0) : -1;
-#pragma unroll 2
+#pragma unroll kK3Unroll
     for (int ks = 0; ks < kG3KS; ++ks) {
       const double dv = dsb[ks * 32];
       double bf[NT];
