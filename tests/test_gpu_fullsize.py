@@ -76,3 +76,26 @@ def test_fullsize_batch_independence(full):
     cfg, prob, basis, sel, plan, params, res = full
     part = online.solve_params(plan, params[100:357])
     assert np.array_equal(part.coefficients, res.coefficients[100:357])
+
+
+def test_diffusion3d_pipeline_with_cg_snapshots():
+    """Config 5's operator end to end at a reduced grid (48^3): GPU CG snapshot
+    solves with the reference's residual guard, leverage selection, online
+    solve, full-residual checker (K5 DMMA lift + K6) against the oracle."""
+    prob = problems.diffusion3d(grid=48)
+    basis, sel = offline(prob, device=torch.device("cuda:0"), prefer_cg=True)
+    plan = online.precompute_online(prob.system, basis, sel)
+    params = prob.test_params(64)
+    res = online.solve_params(plan, params)
+    assert np.all(res.status == 0)
+    for k in (0, 31, 63):
+        c, floor = _oracle(prob, basis, sel, params[k])
+        d = np.linalg.norm(res.coefficients[k] - c) / np.linalg.norm(c)
+        assert d <= max(1e-10, 10 * floor)
+    rr = online.relative_residual(plan, params[:8], res.coefficients[:8])
+    for k in range(0, 8, 3):
+        a = prob.system.matrix(params[k])
+        x = basis.basis @ res.coefficients[k]
+        ref = online_ref.relative_residual(a, x, prob.system.full_rhs(params[k]))
+        assert rr[k] == pytest.approx(ref, rel=1e-3)
+    assert np.median(rr) < 1e-2  # the snapshot basis actually approximates the solutions
