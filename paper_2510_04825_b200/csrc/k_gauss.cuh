@@ -1,7 +1,9 @@
 // K3: Gaussian-kernel row contraction for a batch of bandwidths p.
 //
 //   M_p[i][j] = sum_l E_p(i,l) X[l][j],
-//   E_p(i,l)  = exp(-(D[i][l] * inv_p)) (+ ridge if l == S_i),  inv_p = 1/(2 p p)
+//   E_p(i,l)  = exp(-(D[i][l] * inv_p)) (+ lam if l == S_i),  inv_p = 1/(2 sigma^2)
+//   p = sigma with a plan ridge lam, or p = (lam, sigma) as in the reference's
+//   KRR system (systems.py:423-463)
 //
 // This is what the reference computes per p with the dense detour
 //   online._sampled_rows -> rows_dense -> row_fn -> @ basis.basis
@@ -143,14 +145,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 
 template <int NT>
 __host__ __device__ constexpr size_t gauss3_smem_bytes(int rows_cta) {
-  return (size_t)kG3Stages * (rows_cta / 8 + NT) * kG3KS * 32 * sizeof(double) + 2048 * sizeof(double) +
+  return (size_t)kG3Stages * (rows_cta / 8 + NT) * kG3KS * 32 * sizeof(double) + (2048 + 8) * sizeof(double) +
          2 * kG3Stages * sizeof(uint64_t);
 }
 
 template <int NT, int PW, int MINB>
 __global__ void __launch_bounds__(32 * kGaussMaxWarps, MINB)
 k_gauss_rows3(const double* __restrict__ Df, const double* __restrict__ Xf, const int64_t* __restrict__ S,
-              const double* __restrict__ params, int64_t P, int s, int64_t nchunks, int r, double ridge,
+              const double* __restrict__ params, int dp, int64_t P, int s, int64_t nchunks, int r, double ridge,
               double* __restrict__ Mout) {
   extern __shared__ __align__(128) double gsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -159,7 +161,7 @@ k_gauss_rows3(const double* __restrict__ Df, const double* __restrict__ Xf, cons
   const int row0 = blockIdx.y * rows_cta;
   const int stage_d = (nrg + NT) * kG3KS * 32;  // doubles per stage
   double* tab_s = gsm + (size_t)kG3Stages * stage_d;
-  uint64_t* full = reinterpret_cast<uint64_t*>(tab_s + 2048);
+  uint64_t* full = reinterpret_cast<uint64_t*>(tab_s + 2048 + 8);
   uint64_t* empty = full + kG3Stages;
   const unsigned dbytes = (unsigned)(nrg * kG3KS * 32 * sizeof(double));
   const unsigned xbytes = (unsigned)(NT * kG3KS * 32 * sizeof(double));
@@ -186,17 +188,24 @@ k_gauss_rows3(const double* __restrict__ Df, const double* __restrict__ Xf, cons
   if (threadIdx.x == 0)
     for (int64_t c = 0; c < kG3Stages - 1 && c < nchunks; ++c) issue(c);
 
+  // parameter value = bandwidth sigma (dp == 1, plan ridge) or (lambda, sigma)
+  // (dp == 2, the reference's KRR system, systems.py:423-463)
   const int64_t pbase = (int64_t)blockIdx.x * PW;
   double ninv[PW];
 #pragma unroll
   for (int u = 0; u < PW; ++u) {
     const int64_t p = pbase + u;
-    const double sg = (p < P) ? params[p] : 1.0;
+    const double sg = (p < P) ? params[p * dp + dp - 1] : 1.0;
     ninv[u] = -(1.0 / (2.0 * sg * sg));  // reference: inv = 1.0 / (2.0 * sigma * sigma)
   }
+  if (threadIdx.x < PW) {
+    const int64_t p = pbase + threadIdx.x;
+    const double lam = (dp == 2) ? ((p < P) ? params[p * 2] : 0.0) : ridge;
+    tab_s[2048 + threadIdx.x] = 1.0 + lam;  // the reference's exp(-0) + lam (_kernels.py:49)
+  }
+  __syncthreads();
   const int grow = row0 + warp * 8 + (lane >> 2);
   const int64_t srow = (grow < s) ? S[grow] : -1;
-  const double onepr = 1.0 + ridge;  // the reference's exp(-0) + lam (_kernels.py:49)
 
   double acc[PW][NT][2];
 #pragma unroll
@@ -221,7 +230,7 @@ k_gauss_rows3(const double* __restrict__ Df, const double* __restrict__ Xf, cons
       const bool diag = (4 * ks + (lane & 3)) == dcol;
 #pragma unroll
       for (int u = 0; u < PW; ++u) {
-        const double e = sas_exp64_t2k_ridge(dv, ninv[u], tab_s, diag, onepr);
+        const double e = sas_exp64_t2k_ridge(dv, ninv[u], tab_s, diag ? 2048 + u : -1);
 #pragma unroll
         for (int t = 0; t < NT; ++t) dmma884(acc[u][t][0], acc[u][t][1], e, bf[t]);
       }

@@ -168,13 +168,14 @@ __global__ void __launch_bounds__(256) k_resid_affine(const T* __restrict__ X, i
 // re-evaluated on the fly (n^2 exps per p; used on a small subset of p).
 __global__ void __launch_bounds__(256) k_resid_gauss(const double* __restrict__ X, int64_t n, int r,
                                                      const double* __restrict__ pts, int d,
-                                                     double ridge, const double* __restrict__ b,
+                                                     double ridge, int dp, const double* __restrict__ b,
                                                      const double* __restrict__ params,
                                                      const double* __restrict__ xfull,  // P x n (lifted)
                                                      double* __restrict__ part) {
   __shared__ double red[32];
   const int64_t p = blockIdx.y;
-  const double sg = params[p];
+  const double sg = params[p * dp + dp - 1];
+  const double lam = (dp == 2) ? params[p * 2] : ridge;
   const double inv = 1.0 / (2.0 * sg * sg);
   const double* x = xfull + p * n;
   double rr = 0.0, bb = 0.0;
@@ -189,7 +190,7 @@ __global__ void __launch_bounds__(256) k_resid_gauss(const double* __restrict__ 
         dd = __dadd_rn(dd, __dmul_rn(df, df));
       }
       double kv = exp(-(dd * inv));
-      if (l == i) kv += ridge;
+      if (l == i) kv += lam;
       acc = fma(kv, x[l], acc);
     }
     const double res = acc - b[i];

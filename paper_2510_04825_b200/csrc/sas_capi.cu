@@ -240,7 +240,7 @@ __global__ void k_debug_exp64(const double* x, double* y, int64_t n) {
   for (int j = threadIdx.x; j < 2048; j += blockDim.x) tab_s[j] = g_exp2_tab2048[j];
   __syncthreads();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    y[i] = sas_exp64_t2k_ridge(x[i], SAS_INVLN2X2K, tab_s, false, 0.0);
+    y[i] = sas_exp64_t2k_ridge(x[i], SAS_INVLN2X2K, tab_s, -1);
 }
 
 // Device evaluation of the K3 exponential (on t = x * 2048/ln2) for accuracy tests; device pointers.
@@ -279,7 +279,8 @@ extern "C" int sas_plan_create(const sas_desc* desc, const void* X, int64_t n, i
     for (int64_t q = 0; q < (int64_t)s * desc->n_edges; ++q)
       ARG_CHECK(desc->edge_nbr[q] < n, "stencil: neighbour index out of range");
   } else if (desc->op_kind == SAS_OP_GAUSS) {
-    ARG_CHECK(desc->dtype == SAS_F64 && !desc->param_complex && desc->param_dim == 1, "gauss: real scalar bandwidth only");
+    ARG_CHECK(desc->dtype == SAS_F64 && !desc->param_complex && (desc->param_dim == 1 || desc->param_dim == 2),
+              "gauss: real parameters sigma or (lambda, sigma) only");
     ARG_CHECK(desc->points && desc->point_dim >= 1, "gauss: points required");
       } else {
     ARG_CHECK(false, "unknown op_kind %d", desc->op_kind);
@@ -584,8 +585,8 @@ static int launch_gauss3(sas_plan* pl, const double* params, int64_t P, double* 
   SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((unsigned)((P + PW - 1) / PW), (unsigned)gy);
   stage_begin(pl, st, SAS_STAGE_GAUSS_ROWS);
-  kern<<<grid, 32 * nw, smem, st>>>(pl->Dfrag, pl->Xfrag, pl->S, params, P, pl->s, pl->n_pad / kGaussKC, pl->r,
-                                    pl->ridge, Mout);
+  kern<<<grid, 32 * nw, smem, st>>>(pl->Dfrag, pl->Xfrag, pl->S, params, pl->dp, P, pl->s, pl->n_pad / kGaussKC,
+                                    pl->r, pl->ridge, Mout);
   stage_end(pl, st);
   SAS_CUDA_CHECK(cudaGetLastError());
   pl->last_launches++;
@@ -914,7 +915,7 @@ extern "C" int sas_residual(sas_plan* pl, const void* params, const void* coef, 
     double* xs = nullptr;
     if ((rc = dalloc(&xs, (size_t)P * pl->n * sizeof(double)))) return rc;
     if ((rc = launch_lift_dmma(pl, (const double*)coef, P, xs, st))) { cudaFree(xs); return rc; }
-    k_resid_gauss<<<grid, 256, 0, st>>>((const double*)pl->X, pl->n, pl->r, pl->pts, pl->pdim, pl->ridge,
+    k_resid_gauss<<<grid, 256, 0, st>>>((const double*)pl->X, pl->n, pl->r, pl->pts, pl->pdim, pl->ridge, pl->dp,
                                         (const double*)pl->full_b, (const double*)params, xs, pl->rpart);
     cudaError_t e = cudaStreamSynchronize(st);
     cudaFree(xs);

@@ -270,7 +270,7 @@ __device__ __forceinline__ double sas_exp64_t2k(double x, const double* __restri
 #define SAS_EXP2K_A3 0x1.c6b08d704a0c0p-38
 
 __device__ __forceinline__ double sas_exp64_t2k_ridge(double a, double b, const double* __restrict__ tab_s,
-                                                      bool diag, double onepr) {
+                                                      int ridx) {
   const double kd = fma(a, b, SAS_EXP_MAGIC);
   const int ki = __double2loint(kd);
   const double kf = __dsub_rn(kd, SAS_EXP_MAGIC);
@@ -278,7 +278,7 @@ __device__ __forceinline__ double sas_exp64_t2k_ridge(double a, double b, const 
   double q = fma(r, SAS_EXP2K_A3, SAS_EXP2K_A2);
   q = fma(q, r, SAS_EXP2K_A1);
   q = q * r;
-  const double tv = diag ? onepr : tab_s[ki & 2047];
+  const double tv = tab_s[ridx >= 0 ? ridx : (ki & 2047)];
   const double res = fma(tv, q, tv);
   const int hi = __double2hiint(res) + ((ki >> 11) << 20);
   const int keep = (ki >= SAS_EXP2K_KMIN) ? -1 : 0;

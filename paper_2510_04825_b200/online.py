@@ -401,10 +401,70 @@ def solve_batch(plan: OnlinePlan, parameters, want_interval: bool = False, worke
     return rows
 
 
-def solve_apsnap(system, basis, p):
-    """Not on the online path: the full O(n r'^2) least squares stays in the
-    reference (online.py:156-165)."""
-    raise NotImplementedError("solve_apsnap is not part of the GPU online path; use subapsnap.online.solve_apsnap")
+def _operator_times_basis(system, X, p, dev):
+    """B = A(p) X on the GPU (torch), for the full least squares of solve_apsnap."""
+    import torch
+    op = getattr(system, "operator", None)
+    if system.affine_terms is not None:
+        cdt = torch.complex128 if X.is_complex() or np.iscomplexobj(p) else torch.float64
+        B = torch.zeros(X.shape, dtype=cdt, device=dev)
+        for t in system.affine_terms:
+            m = t.matrix.tocsr()
+            A = torch.sparse_csr_tensor(torch.from_numpy(m.indptr.astype(np.int64)),
+                                        torch.from_numpy(m.indices.astype(np.int64)),
+                                        torch.from_numpy(m.data.astype(np.complex128 if cdt == torch.complex128
+                                                                       else np.float64)),
+                                        size=m.shape, device=dev)
+            f = complex(t.coeff(p))
+            B += (f if cdt == torch.complex128 else f.real) * (A @ X.to(cdt))
+        return B
+    if isinstance(op, StencilOperator):
+        nbr, phi = op.edges(np.arange(op.n))
+        pv = torch.tensor(np.asarray(p, dtype=float).ravel(), device=dev)
+        ph = torch.from_numpy(phi).to(dev)
+        arg = ph[..., 0] * pv[0]
+        for k in range(1, pv.numel()):
+            arg = arg + ph[..., k] * pv[k]
+        c = torch.exp(arg) / (op.h * op.h)
+        nb = torch.from_numpy(nbr).to(dev)
+        inside = nb >= 0
+        B = c.sum(dim=1, keepdim=True) * X
+        for e in range(nb.shape[1]):
+            idx = torch.where(inside[:, e], nb[:, e], torch.zeros_like(nb[:, e]))
+            B -= (c[:, e] * inside[:, e])[:, None] * X[idx]
+        return B
+    if isinstance(op, GaussianKernelOperator):
+        pts = torch.from_numpy(op.points).to(dev)
+        lam, sg = (float(p[0]), float(p[1])) if op.ridge_from_param else (op.ridge, float(p))
+        D = torch.zeros((op.n, op.n), dtype=torch.float64, device=dev)
+        for k in range(pts.shape[1]):
+            df = pts[:, k][:, None] - pts[:, k][None, :]
+            D += df * df
+        K = torch.exp(-(D * (1.0 / (2.0 * sg * sg))))
+        K.diagonal().add_(lam)
+        return K @ X
+    raise ValueError("system has no GPU operator")
+
+
+def solve_apsnap(system, basis, p, device: int = 0):
+    """Full least squares min ||A(p) Q_X c - b(p)|| (online.py:156-165) on the
+    GPU: B = A(p) X from the GPU operator, Householder QR (cuSOLVER via
+    torch.linalg.qr), the reference's 1e-12 rank test (linalg.py:107-112) and a
+    triangular solve.  Returns (coefficients, true residual norm).  Not on the
+    online hot path: O(n r'^2) per parameter."""
+    import torch
+    dev = torch.device(f"cuda:{device}")
+    X = torch.from_numpy(np.ascontiguousarray(basis.basis)).to(dev)
+    B = _operator_times_basis(system, X, p, dev)
+    rhs = torch.from_numpy(np.ascontiguousarray(np.asarray(system.full_rhs(p)))).to(dev).to(B.dtype)
+    q, rmat = torch.linalg.qr(B, mode="reduced")
+    diag = rmat.diagonal().abs()
+    if diag.numel() and float(diag.min()) < 1e-12 * max(float(diag.max()), np.finfo(float).tiny):
+        raise RankDeficiencyError(f"rank-deficient least-squares matrix at column {int(diag.argmin())}")
+    y = q.conj().transpose(0, 1) @ rhs
+    coeff = torch.linalg.solve_triangular(rmat, y[:, None], upper=True)[:, 0]
+    residual = float(torch.linalg.norm(B @ coeff - rhs))
+    return coeff.cpu().numpy(), residual
 
 
 # --------------------------------------------------------------------------

@@ -178,10 +178,14 @@ class StencilOperator:
 @dataclass(frozen=True)
 class GaussianKernelOperator:
     """Rows of K_p + ridge I, K_p(i,j) = exp(-(D_ij * inv)), D_ij = sum_k
-    (x_ik - x_jk)^2 summed sequentially over k, inv = 1/(2 p p), p the bandwidth."""
+    (x_ik - x_jk)^2 summed sequentially over k, inv = 1/(2 sigma^2).  The
+    parameter is the bandwidth sigma (fixed `ridge`), or with
+    `ridge_from_param` the pair p = (lambda, sigma) of the reference's KRR
+    system (systems.py:423-463, rows by _kernels.rbf_rows for 1-D points)."""
 
     points: np.ndarray
-    ridge: float
+    ridge: float = 0.0
+    ridge_from_param: bool = False
 
     @property
     def n(self) -> int:

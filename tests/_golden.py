@@ -68,6 +68,15 @@ def delay_system(n=200, tau=0.1, kappa=2.1, seed=0):
                             name="delay")
 
 
+def krr_system(t_train, y_train):
+    """The reference's KRR system (systems.py:423-463) as a drop-in system:
+    p = (lambda, sigma), K_sigma + lambda I on 1-D points."""
+    from paper_2510_04825_b200.systems import Axis, Domain
+    op = GaussianKernelOperator(points=np.ascontiguousarray(np.asarray(t_train)[:, None]), ridge_from_param=True)
+    return ParametricSystem(len(t_train), Domain(axes=(Axis(1e-5, 1e2), Axis(0.1, 10.0))), np.asarray(y_train),
+                            operator=op, name="krr")
+
+
 def load(name: str) -> Case:
     d = dict(np.load(GOLDEN / f"{name}.npz"))
     if name.startswith("cfg"):
@@ -77,6 +86,8 @@ def load(name: str) -> Case:
         system = tridiag_system()
     elif name == "delay":
         system = delay_system()
+    elif name == "krr":
+        system = krr_system(d["t_train"], d["y_train"])
     else:
         raise KeyError(name)
     imag = any(a.imag for a in system.domain.axes)
@@ -106,7 +117,10 @@ def oracle_M(case: Case, p):
     else:
         op = sysm.operator
         if isinstance(op, GaussianKernelOperator):
-            fn = lambda q, rows: online_ref.gauss_rows(op.points, rows, float(q), op.ridge)
+            if op.ridge_from_param:
+                fn = lambda q, rows: online_ref.gauss_rows(op.points, rows, float(q[1]), float(q[0]))
+            else:
+                fn = lambda q, rows: online_ref.gauss_rows(op.points, rows, float(q), op.ridge)
             m = online_ref.sampled_rows(fn, X, idx, p)
         else:
             fn = lambda q, rows: online_ref.stencil_rows(op, q, rows).toarray()
@@ -138,8 +152,10 @@ def full_matrix(case: Case, p):
         return sp.csr_matrix(out)
     op = sysm.operator
     if isinstance(op, GaussianKernelOperator):
+        if op.ridge_from_param:
+            return online_ref.gauss_rows(op.points, np.arange(op.n), float(p[1]), float(p[0]))
         return online_ref.gauss_rows(op.points, np.arange(op.n), float(p), op.ridge)
     return online_ref.stencil_rows(op, p, np.arange(op.n))
 
 
-GOLDEN_NAMES = ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "tridiag_lupp", "tridiag_leverage", "delay"]
+GOLDEN_NAMES = ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "tridiag_lupp", "tridiag_leverage", "delay", "krr"]

@@ -142,7 +142,7 @@ def params_array(params):
 
 
 def main(which=None):
-    cfgs = which or [1, 2, 3, 4, 5]
+    cfgs = [c for c in (which or [1, 2, 3, 4, 5]) if isinstance(c, int)]
     for cfg in cfgs:
         prob = problems.build(cfg, **SIZES[cfg])
         params = prob.test_params(COUNTS[cfg])
@@ -168,6 +168,18 @@ def main(which=None):
             res["params"] = params_array(params)
             np.savez_compressed(OUT / f"tridiag_{strat}.npz", **res)
             print(f"tridiag {strat}: r'={res['X'].shape[1]} s={res['S'].size}")
+        # the reference's own KRR system: p = (lambda, sigma), 1-D points,
+        # _kernels.rbf_rows row oracle (test_online.py:159-172)
+        rsys = ref_systems.build_problem(ref_systems.ProblemSpec("krr", {"n_train": 120, "n_test": 10}))
+        pairs = [(1e-3, 1.0), (1e-1, 3.0), (1.0, 6.0), (10.0, 9.0)]
+        rng = np.random.default_rng(5)
+        params = pairs + [(float(10 ** rng.uniform(-3, 1)), float(rng.uniform(1.0, 9.0))) for _ in range(20)]
+        res = run_reference(rsys, pairs, "qr", None, 0, params, oversample=4.0)
+        res["params"] = params_array(params)
+        res["t_train"] = rsys.extras["t_train"]
+        res["y_train"] = rsys.extras["y_train"]
+        np.savez_compressed(OUT / "krr.npz", **res)
+        print(f"krr: r'={res['X'].shape[1]} s={res['S'].size} mode={res['mode']}")
         # delay system: coefficient -exp(tau p) (an "other" term in the reference)
         rsys = ref_systems.build_problem(ref_systems.ProblemSpec("delay", {"n": 200}))
         pts = ref_snapshot.default_snapshot_points(rsys.domain, 8, "log-spaced")

@@ -194,3 +194,32 @@ def test_reference_like_system_with_opaque_coefficient():
     for k in range(len(case.params)):
         d = np.linalg.norm(res.coefficients[k] - ref[k]) / np.linalg.norm(ref[k])
         assert d <= _tol(case, k)
+
+
+@pytest.mark.parametrize("name", ["tridiag_lupp", "cfg1", "cfg4", "cfg3", "krr"])
+def test_solve_apsnap_matches_oracle(name):
+    """solve_apsnap (online.py:156-165): the full least squares on the GPU
+    against the oracle's LAPACK solve of the same A(p) X."""
+    case = load(name)
+    from oracle import online_ref
+    for p in case.params[:3]:
+        c, res = online.solve_apsnap(case.system, case.basis, p)
+        a = full_matrix(case, p)
+        bmat = np.asarray(a @ case.basis.basis)
+        rhs = case.system.full_rhs(p)
+        ref = online_ref.solve_ls(bmat, rhs)
+        assert np.linalg.norm(c - ref) <= 1e-9 * np.linalg.norm(ref)
+        assert res == pytest.approx(np.linalg.norm(bmat @ ref - rhs), rel=1e-6, abs=1e-12 * np.linalg.norm(rhs))
+
+
+def test_full_selector_equals_apsnap():
+    """S = I reproduces the full snapshot least squares (test_online.py:25-35,
+    acceptance criterion 2): the batched online kernel with s = n = 120 rows."""
+    case = load("tridiag_lupp")
+    from paper_2510_04825_b200.offline import RowSelector
+    sel = RowSelector(indices=np.arange(case.system.n), n=case.system.n, strategy="full")
+    plan = online.precompute_online(case.system, case.basis, sel)
+    res = online.solve_params(plan, case.params)
+    for k, p in enumerate(case.params):
+        ref, _ = online.solve_apsnap(case.system, case.basis, p)
+        assert np.linalg.norm(res.coefficients[k] - ref) <= 1e-12 * np.linalg.norm(ref) * 100

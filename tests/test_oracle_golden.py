@@ -17,8 +17,14 @@ def test_oracle_matches_reference(name):
         coef, sres, out = oracle_solve(case, p)
         ref = d["coef"][k]
         # same numpy/LAPACK calls as the reference: agreement at the rounding level
-        assert np.linalg.norm(coef - ref) <= 1e-13 * np.linalg.norm(ref), (name, k)
-        assert abs(sres - d["sres"][k]) <= 1e-12 * max(abs(d["sres"][k]), 1e-300) + 1e-300, (name, k)
+        # (the krr rows come from the reference's numba rbf_rows, whose exp can
+        # differ from numpy's by an ulp, so residuals at the rounding floor are
+        # compared absolutely)
+        tol = max(1e-13, 2.0 * float(d["floor"][k]))
+        assert np.linalg.norm(coef - ref) <= tol * np.linalg.norm(ref), (name, k)
+        t = case.system.rhs(p, case.selector.indices)
+        wt = np.linalg.norm(t * case.selector.weights if case.selector.weights is not None else t)
+        assert abs(sres - d["sres"][k]) <= 1e-12 * abs(d["sres"][k]) + 1e3 * np.finfo(float).eps * wt, (name, k)
         if out is not None:
             assert abs(out - d["outv"][k]) <= 1e-13 * abs(d["outv"][k]) + 1e-300
 
