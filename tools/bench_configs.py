@@ -139,7 +139,11 @@ def run(cfg, steps, dev, synthetic=False, P=None, check=True, resid_count=0):
         resid = {"count": resid_count, "seconds": round(t_rr, 4), "median_relres": float(np.median(rr))}
         if prob.system.n <= 2_000_000:
             x = basis.basis @ coef[0]
-            a = prob.system.matrix(params[0])
+            op = getattr(prob.system, "operator", None)
+            if isinstance(op, GaussianKernelOperator):
+                a = online_ref.gauss_rows(op.points, np.arange(op.n), float(params[0]), op.ridge)
+            else:
+                a = prob.system.matrix(params[0])
             b = prob.system.full_rhs(params[0])
             ref = online_ref.relative_residual(a, x, b)
             resid["relres0_gpu"] = float(rr[0])
