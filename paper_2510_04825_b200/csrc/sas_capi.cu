@@ -542,7 +542,8 @@ static bool lsq_force_cta() {
 // 32/RG column groups) lane layout and RA x CB slots per lane, so it covers
 // s <= W*RG*RA rows and r+1 <= (32/RG)*CB columns.  The table is ordered by
 // cost; the first shape that fits wins (configs 1,2: W=1; config 4 (complex
-// 120x9): W=2; config 3 (160x41): W=6; config 5 (200x51): W=8).  k_lsq (CTA
+// 120x9): W=2; config 3 (160x41): W=8; config 5 (200x51): W=16; measured
+// alternatives in profiles/r01_k4_tuning.txt).  k_lsq (CTA
 // per p, shared-memory partials) is the fallback; SAS_LSQ_KERNEL=cta forces it.
 template <typename T, class Asm>
 static int launch_lsq(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t scratch, cudaStream_t st) {
@@ -555,7 +556,9 @@ static int launch_lsq(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t s
       if (cols <= 12 && s <= 256) return launch_lsq_mw_t<T, 8, 8, 3, 4>(pl, a, as, scratch, st);
       if (cols <= 24 && s <= 256) return launch_lsq_mw_t<T, 8, 8, 6, 4>(pl, a, as, scratch, st);
       if (cols <= 32 && s <= 128) return launch_lsq_mw_t<T, 4, 8, 4, 4>(pl, a, as, scratch, st);
+      if (cols <= 48 && s <= 160) return launch_lsq_mw_t<T, 4, 5, 6, 8>(pl, a, as, scratch, st);
       if (cols <= 48 && s <= 168) return launch_lsq_mw_t<T, 4, 7, 6, 6>(pl, a, as, scratch, st);
+      if (cols <= 56 && s <= 256) return launch_lsq_mw_t<T, 4, 4, 7, 16>(pl, a, as, scratch, st);
       if (cols <= 64 && s <= 224) return launch_lsq_mw_t<T, 4, 7, 8, 8>(pl, a, as, scratch, st);
       if (cols <= 64 && s <= 256) return launch_lsq_mw_t<T, 4, 8, 8, 8>(pl, a, as, scratch, st);
     } else {
