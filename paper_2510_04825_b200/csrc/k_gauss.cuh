@@ -49,7 +49,13 @@ __global__ void k_gauss_dist(const double* __restrict__ pts, const int64_t* __re
   D[(int64_t)i * ld + l] = acc;
 }
 
-constexpr int kGaussKC = 32;            // K chunk (columns l) per pipeline stage
+#ifndef K3_KC
+#define K3_KC 32
+#endif
+#ifndef K3_STAGES
+#define K3_STAGES 3
+#endif
+constexpr int kGaussKC = K3_KC;         // K chunk (columns l) per pipeline stage
 constexpr int kGaussMaxWarps = 10;      // row groups (8 rows each) per CTA -> 320 threads
 // parameter values per CTA: keep PW*NT*2 accumulator doubles <= 24 (2 CTAs/SM)
 template <int NT>
@@ -79,7 +85,7 @@ __host__ __device__ inline void gauss_row_blocks(int s, int* gy, int* rows_cta) 
 #define K3_UNROLL 2
 #endif
 constexpr int kK3Unroll = K3_UNROLL;  // k-steps unrolled per loop iteration
-constexpr int kG3Stages = 3;
+constexpr int kG3Stages = K3_STAGES;
 constexpr int kG3KS = kGaussKC / 4;  // k-steps per chunk
 
 __global__ void k_gauss_pack_dfrag(const double* __restrict__ D, int64_t ldd, int s, int64_t n, int gy,
