@@ -278,10 +278,33 @@ def main():
     h_outv = torch.empty((Pl, 2), dtype=torch.float64).pin_memory()
     h_status = torch.empty(Pl, dtype=torch.int32).pin_memory()
 
-    def e2e_step():
-        rc = g.lib.sas_solve_host(g.handle, _capi.ptr(h_params), Pl, None, None, _capi.ptr(h_coef),
-                                  _capi.ptr(h_sres), _capi.ptr(h_outv), _capi.ptr(h_status), None)
-        _capi.check(rc, "sas_solve_host")
+    if env.world == 1:
+        def e2e_step():
+            rc = g.lib.sas_solve_host(g.handle, _capi.ptr(h_params), Pl, None, None, _capi.ptr(h_coef),
+                                      _capi.ptr(h_sres), _capi.ptr(h_outv), _capi.ptr(h_status), None)
+            _capi.check(rc, "sas_solve_host")
+        gather_rows = Pl
+    else:
+        # N > 1: each rank copies its shard's parameters in, solves, the result rows
+        # are gathered in input order over NCCL and rank 0 reads the full sweep back
+        d_params = torch.empty_like(params_t)
+        n_all = Pl * env.world
+        gathered = torch.empty((n_all, r), dtype=out["coef"].dtype, device=dev)
+        st_all = torch.empty(n_all, dtype=torch.int32, device=dev)
+        h_all = torch.empty((n_all, r), dtype=torch.float64).pin_memory()
+        h_st_all = torch.empty(n_all, dtype=torch.int32).pin_memory()
+
+        def e2e_step():
+            d_params.copy_(h_params, non_blocking=True)
+            online.solve_device(plan, d_params, out, stream)
+            parallel.all_gather_device(gathered, out["coef"])
+            parallel.all_gather_device(st_all, out["status"])
+            if env.rank == 0:
+                h_all.copy_(gathered, non_blocking=True)
+                h_st_all.copy_(st_all, non_blocking=True)
+            torch.cuda.synchronize(dev)
+            h_status.copy_(h_st_all[:Pl] if env.rank == 0 else out["status"])
+        gather_rows = n_all
 
     for _ in range(W):
         e2e_step()
@@ -298,7 +321,10 @@ def main():
     e2e_val = P * env.world * K / e2e_s
     assert int(h_status.sum().item()) == 0
     h2d = pa.nbytes
-    d2h = h_coef.numel() * 8 + h_sres.numel() * 8 + h_outv.numel() * 8 + h_status.numel() * 4
+    if env.world == 1:
+        d2h = h_coef.numel() * 8 + h_sres.numel() * 8 + h_outv.numel() * 8 + h_status.numel() * 4
+    else:  # rank 0 reads back the gathered coefficients and status of the whole sweep
+        d2h = gather_rows * r * 8 + gather_rows * 4
 
     # ---- roofline of the dominant kernel ------------------------------------
     k3 = stage_ms.get(_capi.SAS_STAGE_GAUSS_ROWS, [])
@@ -350,7 +376,9 @@ def main():
                        "offline_s": round(t_off, 2), "plan_s": round(t_plan, 3),
                        "parallelism": f"p-sharded x{env.world}"},
             "e2e": {"value": round(e2e_val, 1), "unit": "p-values/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h), "api": "sas_solve_host (C ABI, pinned host buffers)"},
+                    "d2h_bytes_per_step": int(d2h),
+                    "api": ("sas_solve_host (C ABI, pinned host buffers)" if env.world == 1 else
+                            "pinned H2D of each shard, sas_solve, NCCL all-gather of the rows, D2H on rank 0")},
             "gpu_launches": int(launches),
             "roofline": roofline,
             "cpu_baseline": cpu,

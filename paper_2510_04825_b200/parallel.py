@@ -106,6 +106,20 @@ def gather_rows(local: np.ndarray, P: int, local_rank: int = 0) -> np.ndarray:
     return np.concatenate(rows, axis=0)
 
 
+def all_gather_device(out, local):
+    """All-gather equal-size shards of a device tensor into `out` in rank order
+    (NCCL all_gather_into_tensor on GPUs; a host round trip under gloo)."""
+    import torch
+    import torch.distributed as dist
+    if dist.get_backend() == "nccl":
+        dist.all_gather_into_tensor(out, local.contiguous())
+        return out
+    parts = [torch.empty_like(local, device="cpu") for _ in range(dist.get_world_size())]
+    dist.all_gather(parts, local.cpu())
+    out.copy_(torch.cat(parts, dim=0))
+    return out
+
+
 def max_over_ranks(value: float, local_rank: int = 0) -> float:
     import torch
     import torch.distributed as dist

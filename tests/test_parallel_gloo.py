@@ -40,6 +40,11 @@ def _worker(rank, world, port, out):
     full = parallel.gather_rows(local, P)
     ok_gather = np.array_equal(full, np.array([[p, p * p, -p] for p in params]))
     status = parallel.gather_rows(np.full(len(mine), rank, dtype=np.int32), P)
+    import torch
+    loc = torch.full((4, 3), float(rank))
+    allg = torch.empty((4 * world, 3))
+    parallel.all_gather_device(allg, loc)
+    ok_gather = ok_gather and bool((allg[:4] == 0).all() and (allg[4:] == 1).all())
     t = parallel.max_over_ranks(1.5 + rank)
     parallel.barrier()
     out[rank] = (bool(ok_bcast), bool(ok_gather), float(t), status.tolist())
