@@ -264,7 +264,13 @@ extern "C" int sas_plan_create(const sas_desc* desc, const void* X, int64_t n, i
   ARG_CHECK(desc->param_dim >= 1, "sas_plan_create: param_dim must be >= 1");
   const int ndev_check = [] { int c = 0; cudaGetDeviceCount(&c); return c; }();
   ARG_CHECK(device >= 0 && device < ndev_check, "sas_plan_create: device %d not available (%d devices)", device, ndev_check);
-  if (desc->dtype == SAS_C128) ARG_CHECK(r + 1 <= 64 && s <= 256, "complex plans need r <= 63, s <= 256");
+  if (desc->dtype == SAS_C128) ARG_CHECK(s <= 256, "complex plans need s <= 256");
+  {
+    // the unweighted M(p), R and the rhs stay in shared memory (<= ~200 KB per CTA)
+    const size_t esz = desc->dtype == SAS_C128 ? 16 : 8;
+    ARG_CHECK((size_t)(s + r) * (r + 1) * esz <= 200 * 1024,
+              "s=%d, r=%d: (s + r)(r + 1) elements exceed the per-CTA shared-memory budget", s, r);
+  }
   if (r + 1 > 32) ARG_CHECK(s <= 256, "plans with r >= 32 need s <= 256");
   if (desc->op_kind == SAS_OP_AFFINE) {
     ARG_CHECK(desc->n_terms >= 1 && desc->n_terms <= 16, "affine: need 1..16 terms");
