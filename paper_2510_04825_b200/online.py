@@ -414,7 +414,7 @@ def _operator_times_basis(system, X, p, dev):
                                         torch.from_numpy(m.indices.astype(np.int64)),
                                         torch.from_numpy(m.data.astype(np.complex128 if cdt == torch.complex128
                                                                        else np.float64)),
-                                        size=m.shape, device=dev)
+                                        size=m.shape, device=dev, check_invariants=True)
             f = complex(t.coeff(p))
             B += (f if cdt == torch.complex128 else f.real) * (A @ X.to(cdt))
         return B
