@@ -23,6 +23,13 @@
  * calling thread.  Per-parameter numerical outcomes go to status[]:
  *   SAS_ST_OK, SAS_ST_RANK_DEFICIENT (linalg.py:107-112, RankDeficiencyError),
  *   SAS_ST_NONFINITE (linalg.py:36-37, ValueError "non-finite entries").
+ *
+ * Threading (the reference's solve_online is pure and may be called from many
+ * threads): every call on a plan may come from any host
+ * thread; calls on one plan serialise on the plan, and device work that uses
+ * the plan's scratch buffers is ordered across the callers' streams (a call
+ * on a different stream than the previous one waits for it on the device).
+ * Independent plans run concurrently.
  */
 #ifndef SAS_H_
 #define SAS_H_

@@ -153,6 +153,31 @@ struct sas_plan {
   std::vector<int32_t> ev_stage;
   int nrec = 0;
   int sms = 148;
+  // concurrency: host calls on one plan serialise on `mu`; device work that
+  // touches the plan's scratch is ordered across caller streams by `scr_ev`
+  std::recursive_mutex mu;
+  cudaEvent_t scr_ev = nullptr;
+  cudaStream_t scr_stream = nullptr;
+  bool scr_used = false;
+};
+
+// Holds the plan for one API call.  When the caller's stream differs from the
+// stream of the previous call, that stream first waits for the previous call's
+// device work (the scratch buffers are shared); on exit the call's position in
+// its stream is recorded for the next caller.
+struct PlanUse {
+  sas_plan* pl;
+  cudaStream_t st;
+  std::unique_lock<std::recursive_mutex> lk;
+  PlanUse(sas_plan* p, cudaStream_t s) : pl(p), st(s), lk(p->mu) {
+    if (pl->scr_ev && pl->scr_used && pl->scr_stream != st) cudaStreamWaitEvent(st, pl->scr_ev, 0);
+  }
+  ~PlanUse() {
+    if (pl->scr_ev && cudaEventRecord(pl->scr_ev, st) == cudaSuccess) {
+      pl->scr_stream = st;
+      pl->scr_used = true;
+    }
+  }
 };
 
 struct DevGuard {
@@ -213,6 +238,7 @@ static void plan_free(sas_plan* pl) {
   for (auto* p : pl->csr_ci) cudaFree(p);
   for (auto* p : pl->csr_va) cudaFree(p);
   if (pl->stream) cudaStreamDestroy(pl->stream);
+  if (pl->scr_ev) cudaEventDestroy(pl->scr_ev);
   for (auto e : pl->ev0) cudaEventDestroy(e);
   for (auto e : pl->ev1) cudaEventDestroy(e);
   delete pl;
@@ -422,6 +448,8 @@ extern "C" int sas_plan_create(const sas_desc* desc, const void* X, int64_t n, i
   }
   cudaError_t e = cudaStreamCreateWithFlags(&pl->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) { plan_free(pl); sas_set_error("stream: %s", cudaGetErrorString(e)); return SAS_ERR_CUDA; }
+  e = cudaEventCreateWithFlags(&pl->scr_ev, cudaEventDisableTiming);
+  if (e != cudaSuccess) { plan_free(pl); sas_set_error("event: %s", cudaGetErrorString(e)); return SAS_ERR_CUDA; }
 #undef TRY
   *out = pl;
   return SAS_OK;
@@ -467,6 +495,7 @@ static void stage_end(sas_plan* pl, cudaStream_t st) {
 
 extern "C" int sas_plan_set_timing(sas_plan* pl, int32_t enable) {
   ARG_CHECK(pl, "null plan");
+  std::lock_guard<std::recursive_mutex> lk(pl->mu);
   pl->timing = enable != 0;
   pl->nrec = 0;
   return SAS_OK;
@@ -475,6 +504,7 @@ extern "C" int sas_plan_set_timing(sas_plan* pl, int32_t enable) {
 extern "C" int32_t sas_stage_times(sas_plan* pl, float* ms, int32_t* stage, int32_t cap) {
   if (!pl) return -1;
   DevGuard g(pl->device);
+  std::lock_guard<std::recursive_mutex> lk(pl->mu);
   int n = pl->nrec < cap ? pl->nrec : cap;
   for (int i = 0; i < n; ++i) {
     cudaEventSynchronize(pl->ev1[i]);
@@ -717,12 +747,14 @@ extern "C" int sas_solve(sas_plan* pl, const void* params, int64_t P, const doub
                          int32_t* badcol, void* stream) {
   ARG_CHECK(pl, "null plan");
   ARG_CHECK(P >= 0, "P must be >= 0");
+  DevGuard g(pl->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  std::unique_lock<std::recursive_mutex> lk(pl->mu);
   pl->last_launches = 0;
   pl->nrec = 0;
   if (P == 0) return SAS_OK;
   ARG_CHECK(params && coef && sres && status, "sas_solve: params, coef, sampled_res and status are required");
-  DevGuard g(pl->device);
-  cudaStream_t st = (cudaStream_t)stream;
+  PlanUse use(pl, st);
   if (pl->dtype == SAS_C128)
     return solve_t<cplx>(pl, params, P, coef_table, rhs_table, coef, sres, outv, status, badcol, st);
   return solve_t<double>(pl, params, P, coef_table, rhs_table, coef, sres, outv, status, badcol, st);
@@ -737,6 +769,7 @@ extern "C" int sas_solve_host(sas_plan* pl, const void* params, int64_t P, const
   ARG_CHECK(params && coef && sres && status, "sas_solve_host: params, coef, sampled_res and status are required");
   DevGuard g(pl->device);
   cudaStream_t st = pl->stream;
+  PlanUse use(pl, st);
   const int64_t pbytes = P * pl->dp * (pl->pcomplex ? 16 : 8);
   int rc;
   if ((rc = ensure(&pl->h_params, &pl->h_params_n, pbytes))) return rc;
@@ -798,6 +831,7 @@ extern "C" int sas_lift(sas_plan* pl, const void* coef, int64_t P, void* x, void
   ARG_CHECK(coef && x, "sas_lift: coef and x required");
   DevGuard g(pl->device);
   cudaStream_t st = (cudaStream_t)stream;
+  std::lock_guard<std::recursive_mutex> lk(pl->mu);
   dim3 grid((unsigned)((pl->n + 255) / 256), (unsigned)((P + kLiftPT - 1) / kLiftPT));
   ARG_CHECK(pl->dtype != SAS_C128 || grid.y <= 65535, "sas_lift: P too large for one call (max %d)",
             65535 * kLiftPT);
@@ -818,6 +852,8 @@ extern "C" int sas_plan_set_operator(sas_plan* pl, const int64_t* const* row_ptr
   ARG_CHECK(pl, "null plan");
   ARG_CHECK(b_full, "set_operator: b required");
   DevGuard g(pl->device);
+  std::lock_guard<std::recursive_mutex> lk(pl->mu);
+  if (pl->scr_used) SAS_CUDA_CHECK(cudaEventSynchronize(pl->scr_ev));
   int rc;
   if (pl->full_b) { cudaFree(pl->full_b); pl->full_b = nullptr; }
   if ((rc = dupload(&pl->full_b, b_full, (size_t)pl->n * pl->esz))) return rc;
@@ -874,6 +910,7 @@ extern "C" int sas_residual(sas_plan* pl, const void* params, const void* coef, 
   ARG_CHECK(P <= 65535, "sas_residual: at most 65535 parameter values per call");
   DevGuard g(pl->device);
   cudaStream_t st = (cudaStream_t)stream;
+  PlanUse use(pl, st);
   int nb = (int)((pl->n + 255) / 256);
   if (nb > pl->sms * 4) nb = pl->sms * 4;
   int rc;

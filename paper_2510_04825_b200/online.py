@@ -26,6 +26,7 @@ from __future__ import annotations
 import ctypes as C
 import math
 import time
+import warnings
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -410,11 +411,13 @@ def _operator_times_basis(system, X, p, dev):
         B = torch.zeros(X.shape, dtype=cdt, device=dev)
         for t in system.affine_terms:
             m = t.matrix.tocsr()
-            A = torch.sparse_csr_tensor(torch.from_numpy(m.indptr.astype(np.int64)),
-                                        torch.from_numpy(m.indices.astype(np.int64)),
-                                        torch.from_numpy(m.data.astype(np.complex128 if cdt == torch.complex128
-                                                                       else np.float64)),
-                                        size=m.shape, device=dev, check_invariants=True)
+            with warnings.catch_warnings():  # torch's beta/invariant notices for CSR tensors
+                warnings.filterwarnings("ignore", message="Sparse", category=UserWarning)
+                A = torch.sparse_csr_tensor(torch.from_numpy(m.indptr.astype(np.int64)),
+                                            torch.from_numpy(m.indices.astype(np.int64)),
+                                            torch.from_numpy(m.data.astype(np.complex128 if cdt == torch.complex128
+                                                                           else np.float64)),
+                                            size=m.shape, device=dev, check_invariants=True)
             f = complex(t.coeff(p))
             B += (f if cdt == torch.complex128 else f.real) * (A @ X.to(cdt))
         return B

@@ -61,3 +61,50 @@ def test_batch_sizes_and_order_independence():
     assert np.array_equal(full.coefficients[5:18], part.coefficients)
     rev = online.solve_params(plan, params[::-1])
     assert np.array_equal(full.coefficients, rev.coefficients[::-1])
+
+
+def test_concurrent_callers_on_one_plan():
+    # the reference's solve_online may be called from many threads
+    # (SPEC.md:372-373); here several host threads share one plan, each on its
+    # own stream (device API) or through the host-buffer call
+    import threading
+
+    import torch
+    prob, basis, sel, params = _gauss_case(1500, 80, count=96)
+    plan = online.precompute_online(prob.system, basis, sel)
+    ref = online.solve_params(plan, params)
+    chunks = [params[i::4] for i in range(4)]
+    errors = []
+
+    def device_worker(k):
+        try:
+            st = torch.cuda.Stream()
+            pt = online.device_params(plan, chunks[k])
+            out = online.alloc_outputs(plan, len(chunks[k]))
+            for _ in range(10):
+                with torch.cuda.stream(st):
+                    online.solve_device(plan, pt, out, stream=st)
+                st.synchronize()
+                if not np.array_equal(out["coef"].cpu().numpy(), ref.coefficients[k::4]):
+                    errors.append(("device", k))
+                    return
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(("device", k, repr(e)))
+
+    def host_worker(k):
+        try:
+            for _ in range(10):
+                res = online.solve_params(plan, chunks[k])
+                if not np.array_equal(res.coefficients, ref.coefficients[k::4]):
+                    errors.append(("host", k))
+                    return
+        except Exception as e:  # pragma: no cover
+            errors.append(("host", k, repr(e)))
+
+    threads = [threading.Thread(target=device_worker, args=(k,)) for k in (0, 1)]
+    threads += [threading.Thread(target=host_worker, args=(k,)) for k in (2, 3)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
