@@ -186,29 +186,40 @@ struct AsmStencil {
   const int8_t* gmap;   // s x (E+1)
   double hh;
   const double* params;  // P x dp (real)
-  static size_t scratch_bytes(int s, int E) { return (size_t)s * (E + 1) * sizeof(double); }
+  // per row: edge coefficients (8 doubles), then the coefficient of each
+  // gathered row in G order (8 doubles, zero for padding slots)
+  static size_t scratch_bytes(int s, int) { return (size_t)s * 16 * sizeof(double); }
   template <class Grp>
   __device__ __forceinline__ void operator()(const Grp& g, int64_t p, double* Ms, int ldm, int s, int r,
                                              unsigned char* scratch) const {
     double* cs = reinterpret_cast<double*>(scratch);
     const double* pp = params + p * dp;
     const int E1 = E + 1;
-    // one row per thread: edge coefficients and the diagonal (edge order)
+    // one row per thread: edge coefficients, the diagonal (edge order), then
+    // the signed coefficient of every gathered row
     for (int i = g.rank(); i < s; i += g.size()) {
+      double* ci = cs + i * 16;
       double d = 0.0;
       for (int e = 0; e < E; ++e) {
         const double* ph = phi + ((int64_t)i * E + e) * dp;
         double arg = dmul_exact(pp[0], ph[0]);
         for (int k = 1; k < dp; ++k) arg = dadd_exact(arg, dmul_exact(pp[k], ph[k]));
         const double c = exp(arg) / hh;
-        cs[i * E1 + 1 + e] = c;
+        ci[1 + e] = c;
         d = dadd_exact(d, c);
       }
-      cs[i * E1] = d;
+      ci[0] = d;
+      const int8_t* mp = gmap + i * E1;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int slot = (q < E1) ? mp[q] : -1;
+        ci[8 + q] = (slot < 0) ? 0.0 : (slot == 0 ? d : -ci[slot]);
+      }
     }
     g.sync();
-    // M = rows @ G: the gathered rows are L2-resident; issue the loads of
-    // kUnroll entries before their FMA chains to keep enough loads in flight.
+    // M = rows @ G in ascending column order with FMA (padding slots add
+    // 0 * 0); the gathered rows are L2-resident, the loads of kUnroll entries
+    // are issued before their FMA chains
     constexpr int kUnroll = 4;
     const int total = s * r;
     RowMajorWalk wk(g.rank(), g.size(), r);
@@ -227,19 +238,17 @@ struct AsmStencil {
       }
 #pragma unroll
       for (int t = 0; t < kUnroll; ++t) {
-        if (base + t * g.size() >= total) break;
-        const int i = ii[t];
-        const int8_t* mp = gmap + i * E1;
-        double m = 0.0;
+        if (base + t * g.size() < total) {
+          const double2* a2 = reinterpret_cast<const double2*>(cs + ii[t] * 16 + 8);
+          double m = 0.0;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          if (q >= E1) break;
-          const int slot = mp[q];
-          if (slot < 0) break;
-          const double a = (slot == 0) ? cs[i * E1] : -cs[i * E1 + slot];
-          m = fma(a, gv[t][q], m);
+          for (int q2 = 0; q2 < 4; ++q2) {
+            const double2 a = a2[q2];
+            if (2 * q2 < E1) m = fma(a.x, gv[t][2 * q2], m);
+            if (2 * q2 + 1 < E1) m = fma(a.y, gv[t][2 * q2 + 1], m);
+          }
+          Ms[ii[t] * ldm + jj[t]] = m;
         }
-        Ms[i * ldm + jj[t]] = m;
       }
     }
   }
@@ -253,7 +262,7 @@ __host__ __device__ inline size_t lsq_smem_bytes(int s, int r, int W, int NC, si
   size_t rr = (size_t)r * ldm;
   size_t uni = part > rr ? part : rr;
   size_t n = (size_t)s * ldm + 2 * (size_t)s + 2 * (size_t)ncol + uni + ncol;
-  return n * sizeof(T) + (W + 8) * sizeof(double) + ((scratch + 15) / 16) * 16;
+  return (n * sizeof(T) + (W + 8) * sizeof(double) + 15) / 16 * 16 + ((scratch + 15) / 16) * 16;
 }
 
 template <typename T, int NC, int RPT, class Asm>
@@ -273,7 +282,7 @@ __global__ void __launch_bounds__(512) k_lsq(LsqArgs<T> a, Asm as, size_t scratc
   size_t partsz = (size_t)2 * W * ncol, rr = (size_t)r * ldm;
   T* cvec = part + (partsz > rr ? partsz : rr);
   double* red = reinterpret_cast<double*>(cvec + ncol);
-  unsigned char* scratch = reinterpret_cast<unsigned char*>(red + W + 8);
+  unsigned char* scratch = smem_raw + (reinterpret_cast<unsigned char*>(red + W + 8) - smem_raw + 15) / 16 * 16;
   (void)scratch_bytes;
 
   for (int64_t p = blockIdx.x; p < a.P; p += gridDim.x) {

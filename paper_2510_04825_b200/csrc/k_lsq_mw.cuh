@@ -69,14 +69,25 @@ __device__ __forceinline__ double rcp_nr(double x) {
   return fma(y, e, y);
 }
 
+// shared doubles after the matrix buffers: 16 residual partials, |R_kk| per
+// column (r <= 64), rank-test result (2)
+constexpr int kLsqRedDoubles = 16 + 64 + 2;
+
 template <typename T>
 __host__ __device__ inline size_t lsq_mw_smem_bytes(int s, int r, int W, int CGxCB, size_t scratch) {
   const int ldm = r + 1;
   // Ms (s x ldm), R/y (r x ldm), c (r), R_kk (r),
   // 2 x [row k (CG*CB) + partials (W x CG*CB)]
-  size_t n = (size_t)s * ldm + (size_t)r * ldm + 2 * (size_t)r + 2 * ((size_t)CGxCB + (size_t)W * CGxCB);
+  size_t n = (size_t)s * ldm + (size_t)r * ldm + 2 * (size_t)r + 2 * ((size_t)CGxCB + (size_t)W * CGxCB) +
+             (size_t)CGxCB;
   size_t bytes = (n * sizeof(T) + 15) / 16 * 16;
-  return bytes + 16 * sizeof(double) + (scratch + 15) / 16 * 16;
+  return bytes + kLsqRedDoubles * sizeof(double) + (scratch + 15) / 16 * 16;
+}
+
+// threads per column when the W warp partials are summed: a power of two
+// <= min(W, 32) with TPC * LDP <= 32 * W
+__host__ __device__ constexpr int lsq_tpc(int W, int LDP, int t = 1) {
+  return (2 * t <= W && 2 * t * LDP <= 32 * W && 2 * t <= 32) ? lsq_tpc(W, LDP, 2 * t) : t;
 }
 
 // One Householder step for column k = bk + CG*VK.  With NRG = W*RG a multiple
@@ -94,8 +105,7 @@ struct LsqStep {
 
   template <int VK>
   static __device__ __forceinline__ void run(T (&A)[RA][CB], int k, int bk, int la, int lb, int grg, int warp,
-                                             int r, T* rk_s, T* pt, T* rdiag, double& dmax, double& dmin,
-                                             int& amin) {
+                                             int r, T* rk_s, T* pt, T* sj_s, T* rdiag, double* nrm_s) {
     constexpr int UK = VK / (NRG / CG);
     const int gk = CG * (VK % (NRG / CG)) + bk;  // row group of row k
     // x_i = M_ik for own rows from column group bk (static slot VK)
@@ -121,41 +131,78 @@ struct LsqStep {
       if (la == 0) pt[warp * LDP + lb + CG * v] = acc;
     }
     __syncthreads();
-    if (W > 1) {
-      // column totals of the W warp partials, one thread per column, warp order
-      for (int j = k + threadIdx.x; j <= r; j += blockDim.x) {
-        T g = pt[j];
+    T sj[CB];
+    T beta;
+    if constexpr (W > 1) {
+      // TPC threads per column sum the W warp partials (fixed order: strided
+      // partial sums, then a butterfly), every group also forms g_kk and the
+      // reflector scalars, and publishes w_j = tau (g_j - conj(beta) M_kj)
+      constexpr int TPC = lsq_tpc(W, LDP);
+      const int jc = threadIdx.x / TPC, sub = threadIdx.x % TPC;
+      const int jr = jc < LDP ? jc : LDP - 1;
+      T g = S::zero(), gk = S::zero();
 #pragma unroll
-        for (int w = 1; w < W; ++w) g = S::add(g, pt[w * LDP + j]);
-        pt[j] = g;
+      for (int q = 0; q < (W + TPC - 1) / TPC; ++q) {
+        const int w = sub + q * TPC;
+        if (w < W) {
+          g = S::add(g, pt[w * LDP + jr]);
+          gk = S::add(gk, pt[w * LDP + k]);
+        }
+      }
+#pragma unroll
+      for (int off = 1; off < TPC; off <<= 1) {
+        g = S::add(g, shfl_xor_t(g, off));
+        gk = S::add(gk, shfl_xor_t(gk, off));
+      }
+      if (sub == 0 && jc >= k && jc <= r) {
+        const T alpha = rk_s[k];
+        const double nrm = sqrt(S::re(gk));
+        const double aa = S::abs(alpha);
+        T bt = S::zero();
+        double tau = 0.0;
+        if (nrm != 0.0) {
+          bt = (aa == 0.0) ? S::from(-nrm, 0.0) : S::mulr(alpha, -nrm * rcp_nr(aa));
+          tau = rcp_nr(nrm * (nrm + aa));  // 2 / (v^H v)
+        }
+        sj_s[jc] = (jc > k) ? S::mulr(S::sub(g, S::mul(S::conj(bt), rk_s[jc])), tau) : S::zero();
+        if (jc == k) {
+          rdiag[k] = bt;
+          nrm_s[k] = nrm;
+        }
       }
       __syncthreads();
-    }
-    const double gkk = S::re(pt[k]);
-    const T alpha = rk_s[k];
-    const double nrm = sqrt(gkk);
-    const double aa = S::abs(alpha);
-    T beta;
-    double tau;
-    if (nrm == 0.0) {
-      beta = S::zero();
-      tau = 0.0;
-    } else {
-      beta = (aa == 0.0) ? S::from(-nrm, 0.0) : S::mulr(alpha, -nrm * rcp_nr(aa));
-      tau = rcp_nr(nrm * (nrm + aa));  // 2 / (v^H v)
-    }
-    if (threadIdx.x == 0) rdiag[k] = beta;
-    dmax = fmax(dmax, nrm);
-    if (nrm < dmin) { dmin = nrm; amin = k; }
-    T sj[CB];
+      beta = rdiag[k];
 #pragma unroll
-    for (int v = VK; v < CB; ++v) {
-      const int j = lb + CG * v;
-      const T w = S::mulr(S::sub(pt[j], S::mul(S::conj(beta), rk_s[j])), tau);
-      sj[v] = (v > VK || j > k) ? w : S::zero();  // columns <= k keep their values
+      for (int v = VK; v < CB; ++v) {
+        const int j = lb + CG * v;
+        sj[v] = (j <= r && (v > VK || j > k)) ? sj_s[j] : S::zero();  // columns <= k keep their values
+      }
+    } else {
+      const double gkk = S::re(pt[k]);
+      const T alpha = rk_s[k];
+      const double nrm = sqrt(gkk);
+      const double aa = S::abs(alpha);
+      double tau;
+      if (nrm == 0.0) {
+        beta = S::zero();
+        tau = 0.0;
+      } else {
+        beta = (aa == 0.0) ? S::from(-nrm, 0.0) : S::mulr(alpha, -nrm * rcp_nr(aa));
+        tau = rcp_nr(nrm * (nrm + aa));  // 2 / (v^H v)
+      }
+      if (threadIdx.x == 0) {
+        rdiag[k] = beta;
+        nrm_s[k] = nrm;
+      }
+#pragma unroll
+      for (int v = VK; v < CB; ++v) {
+        const int j = lb + CG * v;
+        const T w = S::mulr(S::sub(pt[j], S::mul(S::conj(beta), rk_s[j])), tau);
+        sj[v] = (v > VK || j > k) ? w : S::zero();  // columns <= k keep their values
+      }
     }
     // v_i: x_i below the pivot, alpha - beta on it, 0 above
-    const T vdiag = S::sub(alpha, beta);
+    const T vdiag = S::sub(rk_s[k], beta);
 #pragma unroll
     for (int u = UK; u < RA; ++u) {
       const T vi = (u == UK && grg == gk) ? vdiag : xg[u];
@@ -168,7 +215,7 @@ struct LsqStep {
 template <typename T, int RG, int RA, int CB, int W, int VK>
 struct LsqColumns {
   static __device__ __forceinline__ void run(T (&A)[RA][CB], int la, int lb, int grg, int warp, int r, T* rowb,
-                                             T* part, T* rdiag, double& dmax, double& dmin, int& amin) {
+                                             T* part, T* sj_s, T* rdiag, double* nrm_s) {
     constexpr int CG = 32 / RG;
     constexpr int LDP = CG * CB;
     if (VK * CG >= r) return;
@@ -178,12 +225,114 @@ struct LsqColumns {
       if (k >= r) break;
       const int buf = k & 1;
       LsqStep<T, RG, RA, CB, W>::template run<VK>(A, k, bk, la, lb, grg, warp, r, rowb + buf * LDP,
-                                                  part + (size_t)buf * W * LDP, rdiag, dmax, dmin, amin);
+                                                  part + (size_t)buf * W * LDP, sj_s, rdiag, nrm_s);
     }
     if constexpr (VK + 1 < CB)
-      LsqColumns<T, RG, RA, CB, W, VK + 1>::run(A, la, lb, grg, warp, r, rowb, part, rdiag, dmax, dmin, amin);
+      LsqColumns<T, RG, RA, CB, W, VK + 1>::run(A, la, lb, grg, warp, r, rowb, part, sj_s, rdiag, nrm_s);
   }
 };
+
+// Per-parameter outcome when M(p) has non-finite entries (linalg.py:36-37).
+template <typename T>
+__device__ __forceinline__ void lsq_nonfinite(const LsqArgs<T>& a, int64_t p) {
+  using S = Sc<T>;
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  for (int j = threadIdx.x; j < a.r; j += blockDim.x) a.coef[p * a.r + j] = S::from(qnan, 0.0);
+  if (threadIdx.x == 0) {
+    a.status[p] = 2;
+    a.sres[p] = qnan;
+    if (a.badcol) a.badcol[p] = -1;
+    if (a.outv) { a.outv[2 * p] = qnan; a.outv[2 * p + 1] = qnan; }
+  }
+  __syncthreads();
+}
+
+// After the factorisation (strict upper R and y = (Q^H t_w)[:r] in Rs, R_kk
+// in rdiag, |R_kk| in nrm_s): rank test, back substitution, sampled residual
+// and output value for parameter p.  All threads of the CTA call it.
+template <typename T>
+__device__ __forceinline__ void lsq_finish(const LsqArgs<T>& a, int64_t p, const T* Ms, int ldm, const T* Rs,
+                                           T* cvec, const T* rdiag, const double* nrm_s, double* rinfo,
+                                           double* red, int W) {
+  using S = Sc<T>;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = a.s, r = a.r;
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  if (warp == 0) {
+    // rank test on |R_kk| (linalg.py:107-112): the first column of the minimum
+    double mx = 0.0, mn = DBL_MAX;
+    int am = 0x7fffffff;
+    for (int j = lane; j < r; j += 32) {
+      const double d = nrm_s[j];
+      mx = fmax(mx, d);
+      if (d < mn) { mn = d; am = j; }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+      const double pm = __shfl_xor_sync(0xffffffffu, mn, off);
+      const int pa = __shfl_xor_sync(0xffffffffu, am, off);
+      if (pm < mn || (pm == mn && pa < am)) { mn = pm; am = pa; }
+    }
+    if (lane == 0) {
+      rinfo[0] = (r > 0 && mn < 1e-12 * fmax(mx, DBL_MIN)) ? 1.0 : 0.0;
+      rinfo[1] = (double)(am == 0x7fffffff ? 0 : am);
+    }
+  }
+  __syncthreads();
+  const bool rankdef = rinfo[0] != 0.0;
+  const int amin = (int)rinfo[1];
+  if (warp == 0) {
+    if (!rankdef) {
+      // reciprocals of the diagonal in parallel, then a column sweep
+      const T one = S::from(1.0, 0.0);
+      const T rinv0 = (lane < r) ? S::div(one, rdiag[lane]) : S::zero();
+      const T rinv1 = (lane + 32 < r) ? S::div(one, rdiag[lane + 32]) : S::zero();
+      T y0 = (lane < r) ? Rs[lane * ldm + r] : S::zero();
+      T y1 = (lane + 32 < r) ? Rs[(lane + 32) * ldm + r] : S::zero();
+      for (int k = r - 1; k >= 0; --k) {
+        const bool lo = k < 32;
+        T ck = S::mul(lo ? y0 : y1, lo ? rinv0 : rinv1);
+        ck = shfl_t(ck, k & 31);
+        if (lane == 0) cvec[k] = ck;
+        if (lane < k) y0 = S::fms(Rs[lane * ldm + k], ck, y0);
+        if (lane + 32 < k) y1 = S::fms(Rs[(lane + 32) * ldm + k], ck, y1);
+      }
+    } else {
+      for (int j = lane; j < r; j += 32) cvec[j] = S::from(qnan, 0.0);
+    }
+  }
+  __syncthreads();
+  // sampled residual ||w (M c - t)|| from the unweighted M (online.py:121-124)
+  double ss = 0.0;
+  for (int i = threadIdx.x; i < s; i += blockDim.x) {
+    T acc = S::zero();
+    for (int j = 0; j < r; ++j) acc = S::add(acc, S::mul(Ms[i * ldm + j], cvec[j]));
+    T res = S::sub(acc, Ms[i * ldm + r]);
+    if (a.w) res = S::mulr(res, a.w[i]);
+    ss += S::abs2(res);
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
+  if (lane == 0) red[warp] = ss;
+  for (int j = threadIdx.x; j < r; j += blockDim.x) a.coef[p * r + j] = cvec[j];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < W; ++w) tot += red[w];
+    a.sres[p] = rankdef ? qnan : sqrt(tot);
+    a.status[p] = rankdef ? 1 : 0;
+    if (a.badcol) a.badcol[p] = rankdef ? amin : -1;
+    if (a.outv) {
+      T o = S::zero();
+      if (a.proj)
+        for (int j = 0; j < r; ++j) o = S::add(o, S::mul(a.proj[j], cvec[j]));
+      a.outv[2 * p] = S::re(o);
+      a.outv[2 * p + 1] = S::im(o);
+    }
+  }
+  __syncthreads();
+}
 
 template <typename T, int RG, int RA, int CB, int W, class Asm>
 __global__ void __launch_bounds__(32 * W) k_lsq_mw(LsqArgs<T> a, Asm as, size_t scratch_bytes) {
@@ -202,13 +351,15 @@ __global__ void __launch_bounds__(32 * W) k_lsq_mw(LsqArgs<T> a, Asm as, size_t 
   T* rdiag = cvec + r;                // R_kk (beta) per column
   T* rowb = rdiag + r;                // 2 x LDP
   T* part = rowb + 2 * LDP;           // 2 x W x LDP
+  T* sj_s = part + 2 * W * LDP;       // LDP reflector weights w_j
   const size_t core =
-      ((size_t)s * ldm + (size_t)r * ldm + 2 * (size_t)r + 2 * ((size_t)LDP + (size_t)W * LDP)) * sizeof(T);
-  double* red = reinterpret_cast<double*>(smem_raw + (core + 15) / 16 * 16);  // W doubles (<= 8)
-  unsigned char* scratch = smem_raw + (core + 15) / 16 * 16 + 16 * sizeof(double);
+      ((size_t)s * ldm + (size_t)r * ldm + 2 * (size_t)r + 2 * ((size_t)LDP + (size_t)W * LDP) + LDP) * sizeof(T);
+  double* red = reinterpret_cast<double*>(smem_raw + (core + 15) / 16 * 16);  // W residual partials (<= 16)
+  double* nrm_s = red + 16;                                                    // |R_kk|
+  double* rinfo = nrm_s + 64;                                                  // rank deficient, column
+  unsigned char* scratch = smem_raw + (core + 15) / 16 * 16 + kLsqRedDoubles * sizeof(double);
   (void)scratch_bytes;
   const CtaGroup grp;
-  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
 
   for (int64_t p = blockIdx.x; p < a.P; p += gridDim.x) {
     as(grp, p, Ms, ldm, s, r, scratch);
@@ -234,20 +385,11 @@ __global__ void __launch_bounds__(32 * W) k_lsq_mw(LsqArgs<T> a, Asm as, size_t 
       }
     }
     if (__syncthreads_or(bad)) {
-      for (int j = threadIdx.x; j < r; j += blockDim.x) a.coef[p * r + j] = S::from(qnan, 0.0);
-      if (threadIdx.x == 0) {
-        a.status[p] = 2;
-        a.sres[p] = qnan;
-        if (a.badcol) a.badcol[p] = -1;
-        if (a.outv) { a.outv[2 * p] = qnan; a.outv[2 * p + 1] = qnan; }
-      }
-      __syncthreads();
+      lsq_nonfinite<T>(a, p);
       continue;
     }
 
-    double dmax = 0.0, dmin = DBL_MAX;
-    int amin = 0;
-    LsqColumns<T, RG, RA, CB, W, 0>::run(A, la, lb, grg, warp, r, rowb, part, rdiag, dmax, dmin, amin);
+    LsqColumns<T, RG, RA, CB, W, 0>::run(A, la, lb, grg, warp, r, rowb, part, sj_s, rdiag, nrm_s);
 
     // R (strict upper part from registers, diagonal = beta) and y to shared memory
 #pragma unroll
@@ -259,57 +401,6 @@ __global__ void __launch_bounds__(32 * W) k_lsq_mw(LsqArgs<T> a, Asm as, size_t 
         if (i < r && j > i && j <= r) Rs[i * ldm + j] = A[u][v];
       }
     }
-    __syncthreads();
-    const bool rankdef = (r > 0) && (dmin < 1e-12 * fmax(dmax, DBL_MIN));
-    if (warp == 0) {
-      if (!rankdef) {
-        // reciprocals of the diagonal in parallel, then a column sweep
-        const T one = S::from(1.0, 0.0);
-        const T rinv0 = (lane < r) ? S::div(one, rdiag[lane]) : S::zero();
-        const T rinv1 = (lane + 32 < r) ? S::div(one, rdiag[lane + 32]) : S::zero();
-        T y0 = (lane < r) ? Rs[lane * ldm + r] : S::zero();
-        T y1 = (lane + 32 < r) ? Rs[(lane + 32) * ldm + r] : S::zero();
-        for (int k = r - 1; k >= 0; --k) {
-          const bool lo = k < 32;
-          T ck = S::mul(lo ? y0 : y1, lo ? rinv0 : rinv1);
-          ck = shfl_t(ck, k & 31);
-          if (lane == 0) cvec[k] = ck;
-          if (lane < k) y0 = S::fms(Rs[lane * ldm + k], ck, y0);
-          if (lane + 32 < k) y1 = S::fms(Rs[(lane + 32) * ldm + k], ck, y1);
-        }
-      } else {
-        for (int j = lane; j < r; j += 32) cvec[j] = S::from(qnan, 0.0);
-      }
-    }
-    __syncthreads();
-    // sampled residual ||w (M c - t)|| from the unweighted M (online.py:121-124)
-    double ss = 0.0;
-    for (int i = threadIdx.x; i < s; i += blockDim.x) {
-      T acc = S::zero();
-      for (int j = 0; j < r; ++j) acc = S::add(acc, S::mul(Ms[i * ldm + j], cvec[j]));
-      T res = S::sub(acc, Ms[i * ldm + r]);
-      if (a.w) res = S::mulr(res, a.w[i]);
-      ss += S::abs2(res);
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, off);
-    if (lane == 0) red[warp] = ss;
-    for (int j = threadIdx.x; j < r; j += blockDim.x) a.coef[p * r + j] = cvec[j];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double tot = 0.0;
-      for (int w = 0; w < W; ++w) tot += red[w];
-      a.sres[p] = rankdef ? qnan : sqrt(tot);
-      a.status[p] = rankdef ? 1 : 0;
-      if (a.badcol) a.badcol[p] = rankdef ? amin : -1;
-      if (a.outv) {
-        T o = S::zero();
-        if (a.proj)
-          for (int j = 0; j < r; ++j) o = S::add(o, S::mul(a.proj[j], cvec[j]));
-        a.outv[2 * p] = S::re(o);
-        a.outv[2 * p + 1] = S::im(o);
-      }
-    }
-    __syncthreads();
+    lsq_finish<T>(a, p, Ms, ldm, Rs, cvec, rdiag, nrm_s, rinfo, red, W);
   }
 }

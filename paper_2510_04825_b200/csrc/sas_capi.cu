@@ -18,6 +18,7 @@
 #include "sas_common.cuh"
 #include "k_lsq.cuh"
 #include "k_lsq_mw.cuh"
+#include "k_lsq_cw.cuh"
 #include "k_gauss.cuh"
 #include "k_recon.cuh"
 
@@ -294,7 +295,9 @@ extern "C" int sas_plan_create(const sas_desc* desc, const void* X, int64_t n, i
   {
     // the unweighted M(p), R and the rhs stay in shared memory (<= ~200 KB per CTA)
     const size_t esz = desc->dtype == SAS_C128 ? 16 : 8;
-    ARG_CHECK((size_t)(s + r) * (r + 1) * esz <= 200 * 1024,
+    // (stencil rows add 16 coefficient doubles per selected row)
+    const size_t asm_bytes = desc->op_kind == SAS_OP_STENCIL ? (size_t)s * 16 * sizeof(double) : 0;
+    ARG_CHECK((size_t)(s + r) * (r + 1) * esz + asm_bytes <= 200 * 1024,
               "s=%d, r=%d: (s + r)(r + 1) elements exceed the per-CTA shared-memory budget", s, r);
   }
   if (r + 1 > 32) ARG_CHECK(s <= 256, "plans with r >= 32 need s <= 256");
@@ -564,6 +567,67 @@ static int launch_lsq_mw_t(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, siz
   return SAS_OK;
 }
 
+template <int RA, int NCW, int W, class Asm>
+static int launch_lsq_cw_t(sas_plan* pl, const LsqArgs<double>& a, const Asm& as, size_t scratch, cudaStream_t st) {
+  const size_t smem = lsq_cw_smem_bytes(a.s, a.r, RA, scratch);
+  auto kern = k_lsq_cw<RA, NCW, W, Asm>;
+  SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  int occ = 0;
+  SAS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * W, smem));
+  if (occ < 1) {
+    sas_set_error("least-squares kernel does not fit (s=%d r=%d smem=%zu)", a.s, a.r, smem);
+    return SAS_ERR_ARG;
+  }
+  int64_t grid = (int64_t)occ * pl->sms;
+  if (grid > a.P) grid = a.P;
+  if (grid < 1) grid = 1;
+  stage_begin(pl, st, SAS_STAGE_LSQ);
+  kern<<<(unsigned)grid, 32 * W, smem, st>>>(a, as, scratch);
+  stage_end(pl, st);
+  SAS_CUDA_CHECK(cudaGetLastError());
+  pl->last_launches++;
+  return SAS_OK;
+}
+
+// Column-owner variants (rows <= 32*RA, columns <= NCW*W) for real shapes
+// with r+1 > 32, in preference order (config 3: {5,7,6} 5.94 ms vs 6.84 ms
+// for k_lsq_mw; config 5: {7,5,12} 14.5 ms vs 17.6 ms, 32,768 p);
+// SAS_LSQ_CW=<index> forces one (tuning), SAS_LSQ_CW=off disables them.
+struct CwVariant { int ra, ncw, w; };
+static const CwVariant kCwVariants[] = {{5, 7, 6}, {5, 6, 8}, {7, 5, 12}, {7, 4, 16}};
+static int lsq_cw_env() {
+  static int v = -3;
+  if (v == -3) {
+    const char* e = getenv("SAS_LSQ_CW");
+    v = !e ? -1 : (strcmp(e, "off") == 0 ? -2 : atoi(e));
+  }
+  return v;
+}
+template <class Asm>
+static int launch_lsq_cw_idx(sas_plan* pl, const LsqArgs<double>& a, const Asm& as, size_t scratch, cudaStream_t st,
+                             int idx) {
+  switch (idx) {
+    case 0: return launch_lsq_cw_t<5, 7, 6>(pl, a, as, scratch, st);
+    case 1: return launch_lsq_cw_t<5, 6, 8>(pl, a, as, scratch, st);
+    case 2: return launch_lsq_cw_t<7, 5, 12>(pl, a, as, scratch, st);
+    default: return launch_lsq_cw_t<7, 4, 16>(pl, a, as, scratch, st);
+  }
+}
+// returns -1 when no column-owner variant applies
+template <class Asm>
+static int try_lsq_cw(sas_plan* pl, const LsqArgs<double>& a, const Asm& as, size_t scratch, cudaStream_t st) {
+  const int env = lsq_cw_env();
+  if (env == -2) return -1;
+  const int cols = a.r + 1, nv = (int)(sizeof(kCwVariants) / sizeof(kCwVariants[0]));
+  auto fits = [&](int i) { return a.s <= 32 * kCwVariants[i].ra && cols <= kCwVariants[i].ncw * kCwVariants[i].w; };
+  if (env >= 0 && env < nv && fits(env)) return launch_lsq_cw_idx(pl, a, as, scratch, st, env);
+  if (cols <= 32) return -1;
+  for (int i = 0; i < nv; ++i)
+    if (fits(i)) return launch_lsq_cw_idx(pl, a, as, scratch, st, i);
+  return -1;
+}
+
 static bool lsq_force_cta() {
   static int v = -1;
   if (v < 0) {
@@ -578,14 +642,17 @@ static bool lsq_force_cta() {
 // 32/RG column groups) lane layout and RA x CB slots per lane, so it covers
 // s <= W*RG*RA rows and r+1 <= (32/RG)*CB columns.  The table is ordered by
 // cost; the first shape that fits wins (configs 1,2: W=1; config 4 (complex
-// 120x9): W=2; config 3 (160x41): W=8; config 5 (200x51): W=16; measured
-// alternatives in profiles/r01_k4_tuning.txt).  k_lsq (CTA
+// 120x9): W=2; measured alternatives in profiles/r01_k4_tuning.txt).  Real
+// shapes with r+1 > 32 and s <= 224 (configs 3, 5) go to the column-owner
+// kernel k_lsq_cw first (try_lsq_cw).  k_lsq (CTA
 // per p, shared-memory partials) is the fallback; SAS_LSQ_KERNEL=cta forces it.
 template <typename T, class Asm>
 static int launch_lsq(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t scratch, cudaStream_t st) {
   const int cols = a.r + 1, s = a.s;
   if (!lsq_force_cta()) {
     if constexpr (std::is_same<T, double>::value) {
+      const int rc = try_lsq_cw(pl, a, as, scratch, st);
+      if (rc >= 0) return rc;
       if (cols <= 12 && s <= 24) return launch_lsq_mw_t<T, 8, 3, 3, 1>(pl, a, as, scratch, st);
       if (cols <= 12 && s <= 80) return launch_lsq_mw_t<T, 8, 10, 3, 1>(pl, a, as, scratch, st);
       if (cols <= 24 && s <= 80) return launch_lsq_mw_t<T, 8, 10, 6, 1>(pl, a, as, scratch, st);
