@@ -20,8 +20,10 @@
 // (mma.sync.m8n8k4.f64, SASS DMMA.8x8x4 — the only FP64 tensor shape on sm_100a;
 // FP64 has no tcgen05 kind).  D and X fragments stream through a 3-stage
 // shared-memory ring filled by bulk async copies (below) and are reused by all
-// PW parameters of the CTA.  The exp is sas_exp64_t2k (9 FP64-pipe ops; DMMA
-// and DFMA share one FP64 pipe on B200, profiles/r01_fp64_peaks.jsonl).
+// PW parameters of the CTA.  The exp is sas_exp64_t2k_fr (5 FP64-pipe ops, the
+// range reduction on the FP32/integer pipes; DMMA and DFMA share one FP64 pipe
+// on B200, profiles/r01_fp64_peaks.jsonl).  Split-K over n (grid.z) removes the
+// partial last wave (1024 CTAs on 296 slots -> 2048 on 296).
 #pragma once
 #include "sas_common.cuh"
 
@@ -57,14 +59,17 @@ __global__ void k_gauss_dist(const double* __restrict__ pts, const int64_t* __re
 #endif
 constexpr int kGaussKC = K3_KC;         // K chunk (columns l) per pipeline stage
 constexpr int kGaussMaxWarps = 10;      // row groups (8 rows each) per CTA -> 320 threads
+constexpr int kGaussMaxSplit = 2;       // split-K partial products (M scratch is sized for this many)
 // parameter values per CTA: keep PW*NT*2 accumulator doubles <= 24 (2 CTAs/SM)
 template <int NT>
 __host__ __device__ constexpr int gauss_pw() { return NT <= 3 ? 4 : (NT == 4 ? 3 : (NT <= 6 ? 2 : 1)); }
 
-// Row blocking of the s selected rows: gy CTAs along grid.y with rows_cta rows each.
-__host__ __device__ inline void gauss_row_blocks(int s, int* gy, int* rows_cta) {
+// Row blocking of the s selected rows: gy CTAs along grid.y with rows_cta rows
+// each, at most maxw 8-row groups (warps) per CTA (a plan property: the
+// fragment-ordered D is packed per row block).
+__host__ __device__ inline void gauss_row_blocks(int s, int maxw, int* gy, int* rows_cta) {
   const int s_pad = ((s + 7) / 8) * 8;
-  *gy = (s_pad + 8 * kGaussMaxWarps - 1) / (8 * kGaussMaxWarps);
+  *gy = (s_pad + 8 * maxw - 1) / (8 * maxw);
   *rows_cta = 8 * ((s_pad / 8 + *gy - 1) / *gy);
 }
 
@@ -155,11 +160,15 @@ __host__ __device__ constexpr size_t gauss3_smem_bytes(int rows_cta) {
          2 * kG3Stages * sizeof(uint64_t);
 }
 
-template <int NT, int PW, int MINB>
-__global__ void __launch_bounds__(32 * kGaussMaxWarps, MINB)
-k_gauss_rows3(const double* __restrict__ Df, const double* __restrict__ Xf, const int64_t* __restrict__ S,
-              const double* __restrict__ params, int dp, int64_t P, int s, int64_t nchunks, int r, double ridge,
-              double* __restrict__ Mout) {
+// EXPV selects the exponential: 0 = sas_exp64_t2k_ridge (7 FP64-pipe ops),
+// 1 = sas_exp64_t2k_fr (5; FP32/integer range reduction, the default).
+// Split-K: grid.z splits the n chunks into gridDim.z contiguous ranges whose
+// partial products go to Mout + z * msplit; K4 sums them in z order.
+template <int NT, int PW, int MINB, int EXPV, int MAXW>
+__global__ void __launch_bounds__(32 * MAXW, MINB)
+k_gauss_rows(const double* __restrict__ Df, const double* __restrict__ Xf, const int64_t* __restrict__ S,
+             const double* __restrict__ params, int dp, int64_t P, int s, int64_t nchunks, int r, double ridge,
+             double* __restrict__ Mout, int64_t msplit) {
   extern __shared__ __align__(128) double gsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nrg = blockDim.x >> 5;            // row groups = warps
@@ -183,26 +192,31 @@ k_gauss_rows3(const double* __restrict__ Df, const double* __restrict__ Xf, cons
   for (int j = threadIdx.x; j < 2048; j += blockDim.x) tab_s[j] = g_exp2_tab2048[j];
   __syncthreads();
 
-  auto issue = [&](int64_t ch) {
-    const int b = (int)(ch % kG3Stages);
-    if (ch >= kG3Stages) mbar_wait(&empty[b], (unsigned)(((ch / kG3Stages) - 1) & 1));
+  const int64_t c0 = nchunks * blockIdx.z / gridDim.z, nloc = nchunks * (blockIdx.z + 1) / gridDim.z - c0;
+  Mout += blockIdx.z * msplit;
+  auto issue = [&](int64_t j) {  // local chunk j = chunk c0 + j into slot j mod stages
+    const int b = (int)(j % kG3Stages);
+    if (j >= kG3Stages) mbar_wait(&empty[b], (unsigned)(((j / kG3Stages) - 1) & 1));
     double* dst = gsm + (size_t)b * stage_d;
+    const int64_t ch = c0 + j;
     mbar_expect_tx(&full[b], dbytes + xbytes);
     bulk_g2s(dst, dsrc + ch * (int64_t)nrg * kG3KS * 32, dbytes, &full[b]);
     bulk_g2s(dst + nrg * kG3KS * 32, Xf + ch * (int64_t)NT * kG3KS * 32, xbytes, &full[b]);
   };
   if (threadIdx.x == 0)
-    for (int64_t c = 0; c < kG3Stages - 1 && c < nchunks; ++c) issue(c);
+    for (int64_t j = 0; j < kG3Stages - 1 && j < nloc; ++j) issue(j);
 
   // parameter value = bandwidth sigma (dp == 1, plan ridge) or (lambda, sigma)
   // (dp == 2, the reference's KRR system, systems.py:423-463)
   const int64_t pbase = (int64_t)blockIdx.x * PW;
   double ninv[PW];
+  float ninvf[PW];
 #pragma unroll
   for (int u = 0; u < PW; ++u) {
     const int64_t p = pbase + u;
     const double sg = (p < P) ? params[p * dp + dp - 1] : 1.0;
     ninv[u] = -(1.0 / (2.0 * sg * sg));  // reference: inv = 1.0 / (2.0 * sigma * sigma)
+    ninvf[u] = (float)ninv[u];
   }
   if (threadIdx.x < PW) {
     const int64_t p = pbase + threadIdx.x;
@@ -219,10 +233,11 @@ k_gauss_rows3(const double* __restrict__ Df, const double* __restrict__ Xf, cons
 #pragma unroll
     for (int t = 0; t < NT; ++t) acc[u][t][0] = acc[u][t][1] = 0.0;
 
-  for (int64_t ch = 0; ch < nchunks; ++ch) {
-    if (threadIdx.x == 0 && ch + kG3Stages - 1 < nchunks) issue(ch + kG3Stages - 1);
-    const int b = (int)(ch % kG3Stages);
-    mbar_wait(&full[b], (unsigned)((ch / kG3Stages) & 1));
+  for (int64_t j = 0; j < nloc; ++j) {
+    if (threadIdx.x == 0 && j + kG3Stages - 1 < nloc) issue(j + kG3Stages - 1);
+    const int b = (int)(j % kG3Stages);
+    mbar_wait(&full[b], (unsigned)((j / kG3Stages) & 1));
+    const int64_t ch = c0 + j;
     const double* dsb = gsm + (size_t)b * stage_d + warp * kG3KS * 32 + lane;
     const double* xsb = gsm + (size_t)b * stage_d + nrg * kG3KS * 32 + lane;
     const int64_t l0 = ch * kGaussKC;
@@ -236,7 +251,8 @@ k_gauss_rows3(const double* __restrict__ Df, const double* __restrict__ Xf, cons
       const bool diag = (4 * ks + (lane & 3)) == dcol;
 #pragma unroll
       for (int u = 0; u < PW; ++u) {
-        const double e = sas_exp64_t2k_ridge(dv, ninv[u], tab_s, diag ? 2048 + u : -1);
+        const double e = EXPV ? sas_exp64_t2k_fr(dv, ninv[u], ninvf[u], tab_s, diag ? 2048 + u : -1)
+                              : sas_exp64_t2k_ridge(dv, ninv[u], tab_s, diag ? 2048 + u : -1);
 #pragma unroll
         for (int t = 0; t < NT; ++t) dmma884(acc[u][t][0], acc[u][t][1], e, bf[t]);
       }
@@ -252,9 +268,9 @@ k_gauss_rows3(const double* __restrict__ Df, const double* __restrict__ Xf, cons
       double* out = Mout + (p * s + grow) * (int64_t)r;
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
-        const int c0 = t * 8 + 2 * (lane & 3);
-        if (c0 < r) out[c0] = acc[u][t][0];
-        if (c0 + 1 < r) out[c0 + 1] = acc[u][t][1];
+        const int c0c = t * 8 + 2 * (lane & 3);
+        if (c0c < r) out[c0c] = acc[u][t][0];
+        if (c0c + 1 < r) out[c0c + 1] = acc[u][t][1];
       }
     }
   }

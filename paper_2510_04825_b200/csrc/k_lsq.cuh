@@ -90,14 +90,20 @@ struct RowMajorWalk {
 // ---------------------------------------------------------------------------
 template <typename T>
 struct AsmGlobal {
-  const T* M;  // P x s x r
+  const T* M;          // nsplit x P x s x r: split-K partial products (K3), summed in split order
+  int nsplit = 1;
+  int64_t split = 0;   // elements between partials
   static constexpr size_t scratch_bytes(int, int) { return 0; }
   template <class Grp>
   __device__ __forceinline__ void operator()(const Grp& g, int64_t p, T* Ms, int ldm, int s, int r,
                                              unsigned char*) const {
     const T* src = M + p * (int64_t)s * r;
     RowMajorWalk wk(g.rank(), g.size(), r);
-    for (int idx = g.rank(); idx < s * r; idx += g.size(), wk.next()) Ms[wk.i * ldm + wk.j] = src[idx];
+    for (int idx = g.rank(); idx < s * r; idx += g.size(), wk.next()) {
+      T v = src[idx];
+      for (int z = 1; z < nsplit; ++z) v = v + src[idx + z * split];
+      Ms[wk.i * ldm + wk.j] = v;
+    }
   }
 };
 

@@ -86,6 +86,46 @@ double sas_exp64_host(double x) {
   return (ki >= SAS_EXP2K_KMIN) ? res : 0.0;
 }
 
+// Host mirror of sas_exp64_t2k_fr (a >= 0, b < 0), bit for bit.
+static double sas_exp64_fr_host(double a, double b) {
+  const float bf = (float)b;
+  uint64_t abits;
+  memcpy(&abits, &a, 8);
+  int32_t ah = (int32_t)(abits >> 32);
+  if (ah < 0x38000000) ah = 0x38000000;
+  const uint32_t afb = (uint32_t)(ah - 0x38000000) << 3;
+  float af;
+  memcpy(&af, &afb, 4);
+  volatile float prod = af * bf;
+  const float pf = fmaxf(prod, -3.0e6f);
+  volatile float kd32 = pf + 0x1.8p23f;
+  uint32_t kdb;
+  const float kdv = kd32;
+  memcpy(&kdb, &kdv, 4);
+  const int ki = (int)kdb - 0x4B400000;
+  volatile float kabsf = 0x1.8p23f - kdv;
+  const float kav = kabsf;
+  uint32_t kb;
+  memcpy(&kb, &kav, 4);
+  const uint64_t kbits = ((uint64_t)((kb >> 3) + 0x38000000u) << 32) | (uint64_t)(uint32_t)(kb << 29);
+  double kabs;
+  memcpy(&kabs, &kbits, 8);
+  const double r = fma(a, b, kabs);
+  double q = fma(r, SAS_EXP2K_A3, SAS_EXP2K_A2);
+  q = fma(q, r, SAS_EXP2K_A1);
+  volatile double qv = q * r;
+  q = qv;
+  const double tab = h_exp2_tab2048[ki & 2047];
+  double res = fma(tab, q, tab);
+  int64_t rb;
+  memcpy(&rb, &res, 8);
+  rb += (int64_t)(ki >> 11) << 52;
+  memcpy(&res, &rb, 8);
+  return (ki >= SAS_EXP2K_KMIN) ? res : 0.0;
+}
+
+static int k3_exp();
+
 // ---------------------------------------------------------------------------
 struct sas_plan {
   int device = 0;
@@ -117,7 +157,8 @@ struct sas_plan {
   double ridge = 0.0;
   double* D = nullptr;   // s_pad x n_pad squared distances (zero padded)
   int64_t n_pad = 0;
-  double* Dfrag = nullptr;  // K3 v3 fragment-ordered D
+  double* Dfrag = nullptr;  // K3 fragment-ordered D
+  int k3_maxw = kGaussMaxWarps;  // K3 row block: warps per CTA
   double* Xfrag = nullptr;  // K3 v3 fragment-ordered X^T
   // full operator for the residual checker
   int64_t* full_nbr = nullptr;
@@ -260,20 +301,24 @@ __global__ void k_stencil_gather(const double* __restrict__ X, int r, const int6
 
 extern "C" const char* sas_last_error(void) { return g_err.c_str(); }
 extern "C" const char* sas_version(void) { return "sas 0.1.0 (sm_100a)"; }
-extern "C" double sas_debug_exp64_host(double x) { return sas_exp64_host(x); }
+// The debug exponential is the one K3 uses (SAS_K3_EXP).
+extern "C" double sas_debug_exp64_host(double x) {
+  return k3_exp() ? sas_exp64_fr_host(-x, -SAS_INVLN2X2K) : sas_exp64_host(x);
+}
 
-__global__ void k_debug_exp64(const double* x, double* y, int64_t n) {
+__global__ void k_debug_exp64(const double* x, double* y, int64_t n, int expv) {
   __shared__ double tab_s[2048];
   for (int j = threadIdx.x; j < 2048; j += blockDim.x) tab_s[j] = g_exp2_tab2048[j];
   __syncthreads();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    y[i] = sas_exp64_t2k_ridge(x[i], SAS_INVLN2X2K, tab_s, -1);
+    y[i] = expv ? sas_exp64_t2k_fr(-x[i], -SAS_INVLN2X2K, (float)-SAS_INVLN2X2K, tab_s, -1)
+                : sas_exp64_t2k_ridge(x[i], SAS_INVLN2X2K, tab_s, -1);
 }
 
 // Device evaluation of the K3 exponential (on t = x * 2048/ln2) for accuracy tests; device pointers.
 extern "C" int sas_debug_exp64(const double* x, double* y, int64_t n, void* stream) {
   if (n <= 0) return SAS_OK;
-  k_debug_exp64<<<256, 256, 0, (cudaStream_t)stream>>>(x, y, n);
+  k_debug_exp64<<<256, 256, 0, (cudaStream_t)stream>>>(x, y, n, k3_exp());
   SAS_CUDA_CHECK(cudaGetLastError());
   return SAS_OK;
 }
@@ -422,7 +467,11 @@ extern "C" int sas_plan_create(const sas_desc* desc, const void* X, int64_t n, i
       pl->ridge = desc->ridge;
       TRY(dupload(&pl->pts, desc->points, (size_t)n * pl->pdim * sizeof(double)));
       int gy, rows_cta;
-      gauss_row_blocks(s, &gy, &rows_cta);
+      {
+        const char* e = getenv("SAS_K3_MAXW");  // tuning: warps (8-row groups) per CTA
+        pl->k3_maxw = e ? std::max(1, std::min(kGaussMaxWarps, atoi(e))) : kGaussMaxWarps;
+      }
+      gauss_row_blocks(s, pl->k3_maxw, &gy, &rows_cta);
       const int s_pad = gy * rows_cta;
       const int xr = 8 * ((r + 7) / 8);
       pl->n_pad = ((n + kGaussKC - 1) / kGaussKC) * kGaussKC;
@@ -679,62 +728,104 @@ static int launch_lsq(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t s
   return launch_lsq_t<T, 2, 16>(pl, a, as, scratch, st);
 }
 
-// K3 launch.  PW (parameter values per CTA) and min CTAs/SM per NT; for
-// NT == 3, SAS_K3_VARIANT=<pw>,<minb> overrides them in tuning runs.
-template <int NT, int PW, int MINB>
-static int launch_gauss3(sas_plan* pl, const double* params, int64_t P, double* Mout, cudaStream_t st) {
+// K3 launch: PW (parameter values per CTA) from the accumulator budget
+// (gauss_pw), 2 CTAs/SM, the FP32/integer-reduction exponential, split-K chosen
+// against the wave count.  Tuning: SAS_K3_VARIANT=<pw>,<minb>[,<expv>] for
+// 17 <= r <= 24 (NT == 3), SAS_K3_EXP=0|1, SAS_K3_KSPLIT, SAS_K3_MAXW.
+// Split-K factor: the smallest z in 1..kGaussMaxSplit minimising the wave
+// count ceil(ctas z / slots) / z (a partial last wave of whole-n CTAs costs up
+// to a full wave); SAS_K3_KSPLIT forces it.
+static int gauss_ksplit(int64_t ctas, int64_t slots, int64_t nchunks) {
+  const char* e = getenv("SAS_K3_KSPLIT");
+  if (e) return std::max(1, std::min(kGaussMaxSplit, atoi(e)));
+  int best = 1;
+  double bt = 1e300;
+  for (int z = 1; z <= kGaussMaxSplit; ++z) {
+    if (nchunks < (int64_t)z * kG3Stages) break;
+    const double t = (double)((ctas * z + slots - 1) / slots) / z;
+    if (t < bt - 1e-9) { bt = t; best = z; }
+  }
+  return best;
+}
+
+template <int NT, int PW, int MINB, int EXPV, int MAXW = kGaussMaxWarps>
+static int launch_gauss_k(sas_plan* pl, const double* params, int64_t P, double* Mout, cudaStream_t st,
+                          int* ksplit) {
   int gy, rows_cta;
-  gauss_row_blocks(pl->s, &gy, &rows_cta);
+  gauss_row_blocks(pl->s, pl->k3_maxw, &gy, &rows_cta);
   const int nw = rows_cta / 8;
+  if (nw > MAXW) {
+    sas_set_error("gauss rows: %d warps per CTA exceed the kernel's %d", nw, MAXW);
+    return SAS_ERR_ARG;
+  }
   const size_t smem = gauss3_smem_bytes<NT>(rows_cta);
-  auto kern = k_gauss_rows3<NT, PW, MINB>;
+  auto kern = k_gauss_rows<NT, PW, MINB, EXPV, MAXW>;
   SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((unsigned)((P + PW - 1) / PW), (unsigned)gy);
+  int occ = 0;
+  SAS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * nw, smem));
+  const int64_t nch = pl->n_pad / kGaussKC, ctas = ((P + PW - 1) / PW) * gy;
+  const int z = gauss_ksplit(ctas, (int64_t)std::max(occ, 1) * pl->sms, nch);
+  *ksplit = z;
+  dim3 grid((unsigned)((P + PW - 1) / PW), (unsigned)gy, (unsigned)z);
   stage_begin(pl, st, SAS_STAGE_GAUSS_ROWS);
-  kern<<<grid, 32 * nw, smem, st>>>(pl->Dfrag, pl->Xfrag, pl->S, params, pl->dp, P, pl->s, pl->n_pad / kGaussKC,
-                                    pl->r, pl->ridge, Mout);
+  kern<<<grid, 32 * nw, smem, st>>>(pl->Dfrag, pl->Xfrag, pl->S, params, pl->dp, P, pl->s, nch, pl->r, pl->ridge,
+                                    Mout, P * pl->s * (int64_t)pl->r);
   stage_end(pl, st);
   SAS_CUDA_CHECK(cudaGetLastError());
   pl->last_launches++;
   return SAS_OK;
 }
 
+#ifndef SAS_K3_EXP_DEFAULT
+#define SAS_K3_EXP_DEFAULT 1
+#endif
+static int k3_exp() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SAS_K3_EXP");
+    v = e ? (atoi(e) ? 1 : 0) : SAS_K3_EXP_DEFAULT;
+  }
+  return v;
+}
 static int k3_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("SAS_K3_VARIANT");
     v = 0;
     if (e) {
-      int pw = 0, mb = 0;
-      if (sscanf(e, "%d,%d", &pw, &mb) == 2) v = pw * 10 + mb;
+      int pw = 0, mb = 0, ex = 1;
+      if (sscanf(e, "%d,%d,%d", &pw, &mb, &ex) >= 2) v = pw * 100 + mb * 10 + ex;
     }
   }
   return v;
 }
 
 template <int NT>
-static int launch_gauss_nt(sas_plan* pl, const double* params, int64_t P, double* Mout, cudaStream_t st) {
+static int launch_gauss_nt(sas_plan* pl, const double* params, int64_t P, double* Mout, cudaStream_t st, int* z) {
   if constexpr (NT == 3) {
     switch (k3_variant()) {
-      case 42: return launch_gauss3<3, 4, 2>(pl, params, P, Mout, st);
-      case 23: return launch_gauss3<3, 2, 3>(pl, params, P, Mout, st);
-      case 32: return launch_gauss3<3, 3, 2>(pl, params, P, Mout, st);
+      case 421: return launch_gauss_k<3, 4, 2, 1>(pl, params, P, Mout, st, z);
+      case 420: return launch_gauss_k<3, 4, 2, 0>(pl, params, P, Mout, st, z);
+      case 231: return launch_gauss_k<3, 2, 3, 1>(pl, params, P, Mout, st, z);
+      case 321: return launch_gauss_k<3, 3, 2, 1>(pl, params, P, Mout, st, z);
       default: break;
     }
   }
-  return launch_gauss3<NT, gauss_pw<NT>(), 2>(pl, params, P, Mout, st);
+  constexpr int PW = gauss_pw<NT>();
+  if (k3_exp()) return launch_gauss_k<NT, PW, 2, 1>(pl, params, P, Mout, st, z);
+  return launch_gauss_k<NT, PW, 2, 0>(pl, params, P, Mout, st, z);
 }
 
-static int launch_gauss(sas_plan* pl, const double* params, int64_t P, double* Mout, cudaStream_t st) {
+static int launch_gauss(sas_plan* pl, const double* params, int64_t P, double* Mout, cudaStream_t st, int* z) {
   switch ((pl->r + 7) / 8) {
-    case 1: return launch_gauss_nt<1>(pl, params, P, Mout, st);
-    case 2: return launch_gauss_nt<2>(pl, params, P, Mout, st);
-    case 3: return launch_gauss_nt<3>(pl, params, P, Mout, st);
-    case 4: return launch_gauss_nt<4>(pl, params, P, Mout, st);
-    case 5: return launch_gauss_nt<5>(pl, params, P, Mout, st);
-    case 6: return launch_gauss_nt<6>(pl, params, P, Mout, st);
-    case 7: return launch_gauss_nt<7>(pl, params, P, Mout, st);
-    case 8: return launch_gauss_nt<8>(pl, params, P, Mout, st);
+    case 1: return launch_gauss_nt<1>(pl, params, P, Mout, st, z);
+    case 2: return launch_gauss_nt<2>(pl, params, P, Mout, st, z);
+    case 3: return launch_gauss_nt<3>(pl, params, P, Mout, st, z);
+    case 4: return launch_gauss_nt<4>(pl, params, P, Mout, st, z);
+    case 5: return launch_gauss_nt<5>(pl, params, P, Mout, st, z);
+    case 6: return launch_gauss_nt<6>(pl, params, P, Mout, st, z);
+    case 7: return launch_gauss_nt<7>(pl, params, P, Mout, st, z);
+    case 8: return launch_gauss_nt<8>(pl, params, P, Mout, st, z);
     default:
       sas_set_error("gauss rows: r=%d > 64", pl->r);
       return SAS_ERR_ARG;
@@ -781,11 +872,12 @@ static int solve_t(sas_plan* pl, const void* params, int64_t P, const double* co
         int64_t chunk = (64ll << 20) / per;
         chunk = chunk < 4 ? 4 : (chunk / 4) * 4;
         if (chunk > P) chunk = ((P + 3) / 4) * 4;
-        int rc = ensure(&pl->Mscr, &pl->Mscr_P, chunk * per);
+        int rc = ensure(&pl->Mscr, &pl->Mscr_P, kGaussMaxSplit * chunk * per);
         if (rc) return rc;
         for (int64_t p0 = 0; p0 < P; p0 += chunk) {
           const int64_t pc = (P - p0 < chunk) ? (P - p0) : chunk;
-          rc = launch_gauss(pl, (const double*)params + p0, pc, pl->Mscr, st);
+          int z = 1;
+          rc = launch_gauss(pl, (const double*)params + p0, pc, pl->Mscr, st, &z);
           if (rc) return rc;
           LsqArgs<double> b = a;
           b.P = pc;
@@ -795,7 +887,7 @@ static int solve_t(sas_plan* pl, const void* params, int64_t P, const double* co
           b.outv = outv ? outv + 2 * p0 : nullptr;
           b.status = status + p0;
           b.badcol = badcol ? badcol + p0 : nullptr;
-          AsmGlobal<double> as{pl->Mscr};
+          AsmGlobal<double> as{pl->Mscr, z, pc * pl->s * (int64_t)pl->r};
           rc = launch_lsq<double>(pl, b, as, 0, st);
           if (rc) return rc;
         }

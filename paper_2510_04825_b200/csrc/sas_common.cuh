@@ -285,6 +285,36 @@ __device__ __forceinline__ double sas_exp64_t2k_ridge(double a, double b, const 
   return __hiloint2double(hi & keep, __double2loint(res) & keep);
 }
 
+// Same exponential with the range reduction moved off the FP64 pipe (5
+// FP64-pipe ops instead of 7).  Requires a >= 0 and b < 0 (the kernel rows'
+// argument is always <= 0); bf = (float)b.
+//   k = rint(a*b) from an FP32 product of truncated copies (integer bit ops give
+//   float(a); |k - a*b| <= 1/2 + 2^-22 |a*b|, so |r| <= 0.52 with the clamp below
+//   keeping |k| < 2^22), |k| as an exact double built from the float's bits, then
+//   r = a*b + |k| in one FMA on the exact product, as above.  The polynomial
+//   truncation at |r| = 0.52 is 4e-17.  k = 0 yields |k| = 2^-127 instead of 0,
+//   which perturbs r by 2^-127 (below half an ulp of any nonzero r) and leaves the
+//   diagonal entry (a = 0) exactly the selected table value.
+__device__ __forceinline__ double sas_exp64_t2k_fr(double a, double b, float bf, const double* __restrict__ tab_s,
+                                                   int ridx) {
+  const int ah = max(__double2hiint(a), 0x38000000);
+  const float af = __int_as_float((ah - 0x38000000) << 3);  // float(a) truncated; a < 2^-126 -> 0
+  const float pf = fmaxf(af * bf, -3.0e6f);                  // below KMIN: flushed to 0 at the end
+  const float kd32 = pf + 0x1.8p23f;
+  const int ki = __float_as_int(kd32) - 0x4B400000;          // k = rint(pf)
+  const int kb = __float_as_int(0x1.8p23f - kd32);           // bits of float(|k|), exact
+  const double kabs = __hiloint2double((kb >> 3) + 0x38000000, kb << 29);
+  const double r = fma(a, b, kabs);
+  double q = fma(r, SAS_EXP2K_A3, SAS_EXP2K_A2);
+  q = fma(q, r, SAS_EXP2K_A1);
+  q = q * r;
+  const double tv = tab_s[ridx >= 0 ? ridx : (ki & 2047)];
+  const double res = fma(tv, q, tv);
+  const int hi = __double2hiint(res) + ((ki >> 11) << 20);
+  const int keep = (ki >= SAS_EXP2K_KMIN) ? -1 : 0;
+  return __hiloint2double(hi & keep, __double2loint(res) & keep);
+}
+
 // Host reference of the same algorithm (for the CPU accuracy test).
 double sas_exp64_host(double x);
 
