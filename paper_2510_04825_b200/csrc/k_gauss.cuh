@@ -93,6 +93,15 @@ constexpr int kK3Unroll = K3_UNROLL;  // k-steps unrolled per loop iteration
 constexpr int kG3Stages = K3_STAGES;
 constexpr int kG3KS = kGaussKC / 4;  // k-steps per chunk
 
+// max of non-negative doubles (their bit patterns order like the values)
+__global__ void k_max_nonneg(const double* __restrict__ v, int64_t n, unsigned long long* __restrict__ out) {
+  unsigned long long m = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, (unsigned long long)__double_as_longlong(v[i]));
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
 __global__ void k_gauss_pack_dfrag(const double* __restrict__ D, int64_t ldd, int s, int64_t n, int gy,
                                    int rows_cta, int64_t nchunks, double* __restrict__ Df) {
   const int nrg = rows_cta / 8;
@@ -164,11 +173,11 @@ __host__ __device__ constexpr size_t gauss3_smem_bytes(int rows_cta) {
 // 1 = sas_exp64_t2k_fr (5; FP32/integer range reduction, the default).
 // Split-K: grid.z splits the n chunks into gridDim.z contiguous ranges whose
 // partial products go to Mout + z * msplit; K4 sums them in z order.
-template <int NT, int PW, int MINB, int EXPV, int MAXW>
+template <int NT, int PW, int MINB, int EXPV, int MAXW, int SWP>
 __global__ void __launch_bounds__(32 * MAXW, MINB)
 k_gauss_rows(const double* __restrict__ Df, const double* __restrict__ Xf, const int64_t* __restrict__ S,
              const double* __restrict__ params, int dp, int64_t P, int s, int64_t nchunks, int r, double ridge,
-             double* __restrict__ Mout, int64_t msplit) {
+             double* __restrict__ Mout, int64_t msplit, double dmax, const double* __restrict__ X) {
   extern __shared__ __align__(128) double gsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nrg = blockDim.x >> 5;            // row groups = warps
@@ -226,6 +235,15 @@ k_gauss_rows(const double* __restrict__ Df, const double* __restrict__ Xf, const
   __syncthreads();
   const int grow = row0 + warp * 8 + (lane >> 2);
   const int64_t srow = (grow < s) ? S[grow] : -1;
+  // EXPV 2: CTAs whose largest argument stays above -677 (dmax = max D in table
+  // units) take the fast exponential and add the ridge after the contraction.
+  bool fast = false;
+  if (EXPV == 2) {
+    double bmax = 0.0;
+#pragma unroll
+    for (int u = 0; u < PW; ++u) bmax = fmax(bmax, -ninv[u]);
+    fast = dmax * bmax < SAS_EXP2K_FAST_MAX;
+  }
 
   double acc[PW][NT][2];
 #pragma unroll
@@ -233,32 +251,124 @@ k_gauss_rows(const double* __restrict__ Df, const double* __restrict__ Xf, const
 #pragma unroll
     for (int t = 0; t < NT; ++t) acc[u][t][0] = acc[u][t][1] = 0.0;
 
-  for (int64_t j = 0; j < nloc; ++j) {
-    if (threadIdx.x == 0 && j + kG3Stages - 1 < nloc) issue(j + kG3Stages - 1);
-    const int b = (int)(j % kG3Stages);
-    mbar_wait(&full[b], (unsigned)((j / kG3Stages) & 1));
-    const int64_t ch = c0 + j;
-    const double* dsb = gsm + (size_t)b * stage_d + warp * kG3KS * 32 + lane;
-    const double* xsb = gsm + (size_t)b * stage_d + nrg * kG3KS * 32 + lane;
-    const int64_t l0 = ch * kGaussKC;
-    const int dcol = (srow >= l0 && srow < l0 + kGaussKC) ? (int)(srow - l0) : -1;
+  auto expf = [&](double dv, int u, bool diag) {
+    return EXPV ? sas_exp64_t2k_fr(dv, ninv[u], ninvf[u], tab_s, diag ? 2048 + u : -1)
+                : sas_exp64_t2k_ridge(dv, ninv[u], tab_s, diag ? 2048 + u : -1);
+  };
+  if (EXPV == 2 && fast) {
+    for (int64_t j = 0; j < nloc; ++j) {
+      if (threadIdx.x == 0 && j + kG3Stages - 1 < nloc) issue(j + kG3Stages - 1);
+      const int b = (int)(j % kG3Stages);
+      mbar_wait(&full[b], (unsigned)((j / kG3Stages) & 1));
+      const double* dsb = gsm + (size_t)b * stage_d + warp * kG3KS * 32 + lane;
+      const double* xsb = gsm + (size_t)b * stage_d + nrg * kG3KS * 32 + lane;
 #pragma unroll kK3Unroll
-    for (int ks = 0; ks < kG3KS; ++ks) {
-      const double dv = dsb[ks * 32];
-      double bf[NT];
+      for (int ks = 0; ks < kG3KS; ++ks) {
+        const double dv = dsb[ks * 32];
+        double bf[NT];
 #pragma unroll
-      for (int t = 0; t < NT; ++t) bf[t] = xsb[(t * kG3KS + ks) * 32];
-      const bool diag = (4 * ks + (lane & 3)) == dcol;
+        for (int t = 0; t < NT; ++t) bf[t] = xsb[(t * kG3KS + ks) * 32];
+#pragma unroll
+        for (int u = 0; u < PW; ++u) {
+          const double e = sas_exp64_t2k_fast(dv, ninv[u], ninvf[u], tab_s);
+#pragma unroll
+          for (int t = 0; t < NT; ++t) dmma884(acc[u][t][0], acc[u][t][1], e, bf[t]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[b]);
+    }
+    // the kernel-row ridge: M_p += lam_p X[S_i, :] (split 0 only)
+    if (blockIdx.z == 0 && grow < s) {
+      const double* xrow = X + srow * (int64_t)r;
 #pragma unroll
       for (int u = 0; u < PW; ++u) {
-        const double e = EXPV ? sas_exp64_t2k_fr(dv, ninv[u], ninvf[u], tab_s, diag ? 2048 + u : -1)
-                              : sas_exp64_t2k_ridge(dv, ninv[u], tab_s, diag ? 2048 + u : -1);
+        const double lam = (dp == 2) ? ((pbase + u < P) ? params[(pbase + u) * 2] : 0.0) : ridge;
 #pragma unroll
-        for (int t = 0; t < NT; ++t) dmma884(acc[u][t][0], acc[u][t][1], e, bf[t]);
+        for (int t = 0; t < NT; ++t) {
+          const int c0c = t * 8 + 2 * (lane & 3);
+          if (c0c < r) acc[u][t][0] = fma(lam, xrow[c0c], acc[u][t][0]);
+          if (c0c + 1 < r) acc[u][t][1] = fma(lam, xrow[c0c + 1], acc[u][t][1]);
+        }
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[b]);
+  } else if constexpr (SWP) {
+    // Software-pipelined: the exponentials of k-step kk+1 are evaluated while the
+    // DMMAs of k-step kk (on values computed one step earlier) issue, so no DMMA
+    // waits on a just-computed exp chain.  The last k-step of a chunk reads the
+    // next chunk's first D fragment (two chunks resident, then the first is released).
+    double ecur[PW];
+    if (nloc > 0) {
+      mbar_wait(&full[0], 0u);
+      const double dv = gsm[warp * kG3KS * 32 + lane];
+      const int64_t l0 = c0 * kGaussKC;
+      const bool diag = srow == l0 + (lane & 3);
+#pragma unroll
+      for (int u = 0; u < PW; ++u) ecur[u] = expf(dv, u, diag);
+    }
+    for (int64_t j = 0; j < nloc; ++j) {
+      if (threadIdx.x == 0 && j + kG3Stages - 1 < nloc) issue(j + kG3Stages - 1);
+      const int b = (int)(j % kG3Stages);
+      const double* dsb = gsm + (size_t)b * stage_d + warp * kG3KS * 32 + lane;
+      const double* xsb = gsm + (size_t)b * stage_d + nrg * kG3KS * 32 + lane;
+      const int64_t l0 = (c0 + j) * kGaussKC;
+      const int dcol = (srow >= l0 && srow < l0 + kGaussKC) ? (int)(srow - l0) : -1;
+#pragma unroll
+      for (int ks = 0; ks < kG3KS; ++ks) {
+        double enext[PW];
+        if (ks + 1 < kG3KS) {
+          const double dv = dsb[(ks + 1) * 32];
+          const bool diag = (4 * (ks + 1) + (lane & 3)) == dcol;
+#pragma unroll
+          for (int u = 0; u < PW; ++u) enext[u] = expf(dv, u, diag);
+        } else if (j + 1 < nloc) {
+          const int bn = (int)((j + 1) % kG3Stages);
+          mbar_wait(&full[bn], (unsigned)(((j + 1) / kG3Stages) & 1));
+          const double dv = gsm[(size_t)bn * stage_d + warp * kG3KS * 32 + lane];
+          const bool diag = srow == l0 + kGaussKC + (lane & 3);
+#pragma unroll
+          for (int u = 0; u < PW; ++u) enext[u] = expf(dv, u, diag);
+        }
+        double bf[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) bf[t] = xsb[(t * kG3KS + ks) * 32];
+#pragma unroll
+        for (int u = 0; u < PW; ++u)
+#pragma unroll
+          for (int t = 0; t < NT; ++t) dmma884(acc[u][t][0], acc[u][t][1], ecur[u], bf[t]);
+#pragma unroll
+        for (int u = 0; u < PW; ++u) ecur[u] = enext[u];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[b]);
+    }
+  } else {
+    for (int64_t j = 0; j < nloc; ++j) {
+      if (threadIdx.x == 0 && j + kG3Stages - 1 < nloc) issue(j + kG3Stages - 1);
+      const int b = (int)(j % kG3Stages);
+      mbar_wait(&full[b], (unsigned)((j / kG3Stages) & 1));
+      const int64_t ch = c0 + j;
+      const double* dsb = gsm + (size_t)b * stage_d + warp * kG3KS * 32 + lane;
+      const double* xsb = gsm + (size_t)b * stage_d + nrg * kG3KS * 32 + lane;
+      const int64_t l0 = ch * kGaussKC;
+      const int dcol = (srow >= l0 && srow < l0 + kGaussKC) ? (int)(srow - l0) : -1;
+  #pragma unroll kK3Unroll
+      for (int ks = 0; ks < kG3KS; ++ks) {
+        const double dv = dsb[ks * 32];
+        double bf[NT];
+  #pragma unroll
+        for (int t = 0; t < NT; ++t) bf[t] = xsb[(t * kG3KS + ks) * 32];
+        const bool diag = (4 * ks + (lane & 3)) == dcol;
+  #pragma unroll
+        for (int u = 0; u < PW; ++u) {
+          const double e = expf(dv, u, diag);
+  #pragma unroll
+          for (int t = 0; t < NT; ++t) dmma884(acc[u][t][0], acc[u][t][1], e, bf[t]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[b]);
+    }
   }
   if (grow < s) {
 #pragma unroll

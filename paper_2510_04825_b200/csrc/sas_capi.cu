@@ -124,6 +124,41 @@ static double sas_exp64_fr_host(double a, double b) {
   return (ki >= SAS_EXP2K_KMIN) ? res : 0.0;
 }
 
+// Host mirror of sas_exp64_t2k_fast (|a b| < SAS_EXP2K_FAST_MAX), bit for bit.
+static double sas_exp64_fast_host(double a, double b) {
+  const float bf = (float)b;
+  uint64_t abits;
+  memcpy(&abits, &a, 8);
+  int32_t ah = (int32_t)(abits >> 32);
+  if (ah < 0x38000000) ah = 0x38000000;
+  const uint32_t afb = (uint32_t)ah * 8u + 0x40000000u;
+  float af;
+  memcpy(&af, &afb, 4);
+  volatile float kd32v = fmaf(af, bf, 0x1.8p23f);
+  const float kd32 = kd32v;
+  uint32_t kdb;
+  memcpy(&kdb, &kd32, 4);
+  volatile float kabsf = 0x1.8p23f - kd32;
+  const float kav = kabsf;
+  uint32_t kb;
+  memcpy(&kb, &kav, 4);
+  const uint64_t kbits = ((uint64_t)((kb >> 3) + 0x38000000u) << 32) | (uint64_t)(uint32_t)(kb << 29);
+  double kabs;
+  memcpy(&kabs, &kbits, 8);
+  const double r = fma(a, b, kabs);
+  double q = fma(r, SAS_EXP2K_A3, SAS_EXP2K_A2);
+  q = fma(q, r, SAS_EXP2K_A1);
+  volatile double qv = q * r;
+  q = qv;
+  const double tab = h_exp2_tab2048[kdb & 2047];
+  double res = fma(tab, q, tab);
+  int64_t rb;
+  memcpy(&rb, &res, 8);
+  rb += (int64_t)(((int32_t)kdb >> 11) - (0x4B400000 >> 11)) << 52;
+  memcpy(&res, &rb, 8);
+  return res;
+}
+
 static int k3_exp();
 
 // ---------------------------------------------------------------------------
@@ -159,6 +194,7 @@ struct sas_plan {
   int64_t n_pad = 0;
   double* Dfrag = nullptr;  // K3 fragment-ordered D
   int k3_maxw = kGaussMaxWarps;  // K3 row block: warps per CTA
+  double k3_dmax = 0.0;          // largest squared distance in exp table units (K3 fast-exp test)
   double* Xfrag = nullptr;  // K3 v3 fragment-ordered X^T
   // full operator for the residual checker
   int64_t* full_nbr = nullptr;
@@ -303,6 +339,8 @@ extern "C" const char* sas_last_error(void) { return g_err.c_str(); }
 extern "C" const char* sas_version(void) { return "sas 0.1.0 (sm_100a)"; }
 // The debug exponential is the one K3 uses (SAS_K3_EXP).
 extern "C" double sas_debug_exp64_host(double x) {
+  if (k3_exp() == 2 && -x * SAS_INVLN2X2K < SAS_EXP2K_FAST_MAX)  // the CTA-uniform K3 test, per value
+    return sas_exp64_fast_host(-x * SAS_INVLN2X2K, -1.0);
   return k3_exp() ? sas_exp64_fr_host(-x, -SAS_INVLN2X2K) : sas_exp64_host(x);
 }
 
@@ -311,8 +349,10 @@ __global__ void k_debug_exp64(const double* x, double* y, int64_t n, int expv) {
   for (int j = threadIdx.x; j < 2048; j += blockDim.x) tab_s[j] = g_exp2_tab2048[j];
   __syncthreads();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    y[i] = expv ? sas_exp64_t2k_fr(-x[i], -SAS_INVLN2X2K, (float)-SAS_INVLN2X2K, tab_s, -1)
-                : sas_exp64_t2k_ridge(x[i], SAS_INVLN2X2K, tab_s, -1);
+    y[i] = (expv == 2 && -x[i] * SAS_INVLN2X2K < SAS_EXP2K_FAST_MAX)
+               ? sas_exp64_t2k_fast(-x[i] * SAS_INVLN2X2K, -1.0, -1.0f, tab_s)
+               : expv ? sas_exp64_t2k_fr(-x[i], -SAS_INVLN2X2K, (float)-SAS_INVLN2X2K, tab_s, -1)
+                      : sas_exp64_t2k_ridge(x[i], SAS_INVLN2X2K, tab_s, -1);
 }
 
 // Device evaluation of the K3 exponential (on t = x * 2048/ln2) for accuracy tests; device pointers.
@@ -487,6 +527,18 @@ extern "C" int sas_plan_create(const sas_desc* desc, const void* X, int64_t n, i
       k_gauss_pack_dfrag<<<(unsigned)((totd + 255) / 256), 256>>>(pl->D, pl->n_pad, s, n, gy, rows_cta, nch, pl->Dfrag);
       k_gauss_pack_xfrag<<<(unsigned)((totx + 255) / 256), 256>>>((const double*)pl->X, n, r, xr / 8, nch, pl->Xfrag);
 
+      {
+        unsigned long long* dmx = nullptr;
+        TRY(dalloc(&dmx, sizeof(unsigned long long)));
+        cudaMemset(dmx, 0, sizeof(unsigned long long));
+        k_max_nonneg<<<296, 256>>>(pl->D, totd, dmx);
+        unsigned long long hb = 0;
+        cudaMemcpy(&hb, dmx, sizeof(hb), cudaMemcpyDeviceToHost);
+        cudaFree(dmx);
+        double dm;
+        memcpy(&dm, &hb, sizeof(dm));
+        pl->k3_dmax = dm * SAS_INVLN2X2K * (1.0 + 1e-12);
+      }
       cudaError_t e = cudaDeviceSynchronize();
       cudaFree(pl->D);  // only the fragment-ordered copy is used by the kernel
       pl->D = nullptr;
@@ -731,7 +783,8 @@ static int launch_lsq(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t s
 // K3 launch: PW (parameter values per CTA) from the accumulator budget
 // (gauss_pw), 2 CTAs/SM, the FP32/integer-reduction exponential, split-K chosen
 // against the wave count.  Tuning: SAS_K3_VARIANT=<pw>,<minb>[,<expv>] for
-// 17 <= r <= 24 (NT == 3), SAS_K3_EXP=0|1, SAS_K3_KSPLIT, SAS_K3_MAXW.
+// 17 <= r <= 24 (NT == 3), SAS_K3_EXP=0|1|2 (7-op, FP32-reduction, fast with the
+// ridge added after the contraction), SAS_K3_KSPLIT, SAS_K3_MAXW.
 // Split-K factor: the smallest z in 1..kGaussMaxSplit minimising the wave
 // count ceil(ctas z / slots) / z (a partial last wave of whole-n CTAs costs up
 // to a full wave); SAS_K3_KSPLIT forces it.
@@ -748,7 +801,7 @@ static int gauss_ksplit(int64_t ctas, int64_t slots, int64_t nchunks) {
   return best;
 }
 
-template <int NT, int PW, int MINB, int EXPV, int MAXW = kGaussMaxWarps>
+template <int NT, int PW, int MINB, int EXPV, int MAXW = kGaussMaxWarps, int SWP = 0>
 static int launch_gauss_k(sas_plan* pl, const double* params, int64_t P, double* Mout, cudaStream_t st,
                           int* ksplit) {
   int gy, rows_cta;
@@ -759,7 +812,7 @@ static int launch_gauss_k(sas_plan* pl, const double* params, int64_t P, double*
     return SAS_ERR_ARG;
   }
   const size_t smem = gauss3_smem_bytes<NT>(rows_cta);
-  auto kern = k_gauss_rows<NT, PW, MINB, EXPV, MAXW>;
+  auto kern = k_gauss_rows<NT, PW, MINB, EXPV, MAXW, SWP>;
   SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   SAS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * nw, smem));
@@ -769,7 +822,7 @@ static int launch_gauss_k(sas_plan* pl, const double* params, int64_t P, double*
   dim3 grid((unsigned)((P + PW - 1) / PW), (unsigned)gy, (unsigned)z);
   stage_begin(pl, st, SAS_STAGE_GAUSS_ROWS);
   kern<<<grid, 32 * nw, smem, st>>>(pl->Dfrag, pl->Xfrag, pl->S, params, pl->dp, P, pl->s, nch, pl->r, pl->ridge,
-                                    Mout, P * pl->s * (int64_t)pl->r);
+                                    Mout, P * pl->s * (int64_t)pl->r, pl->k3_dmax, (const double*)pl->X);
   stage_end(pl, st);
   SAS_CUDA_CHECK(cudaGetLastError());
   pl->last_launches++;
@@ -777,13 +830,13 @@ static int launch_gauss_k(sas_plan* pl, const double* params, int64_t P, double*
 }
 
 #ifndef SAS_K3_EXP_DEFAULT
-#define SAS_K3_EXP_DEFAULT 1
+#define SAS_K3_EXP_DEFAULT 2
 #endif
 static int k3_exp() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("SAS_K3_EXP");
-    v = e ? (atoi(e) ? 1 : 0) : SAS_K3_EXP_DEFAULT;
+    v = e ? std::max(0, std::min(2, atoi(e))) : SAS_K3_EXP_DEFAULT;
   }
   return v;
 }
@@ -793,8 +846,8 @@ static int k3_variant() {
     const char* e = getenv("SAS_K3_VARIANT");
     v = 0;
     if (e) {
-      int pw = 0, mb = 0, ex = 1;
-      if (sscanf(e, "%d,%d,%d", &pw, &mb, &ex) >= 2) v = pw * 100 + mb * 10 + ex;
+      int pw = 0, mb = 0, ex = 1, sw = 0;
+      if (sscanf(e, "%d,%d,%d,%d", &pw, &mb, &ex, &sw) >= 2) v = (pw * 100 + mb * 10 + ex) * (sw ? 10 : 1) + (sw ? 1 : 0);
     }
   }
   return v;
@@ -805,6 +858,9 @@ static int launch_gauss_nt(sas_plan* pl, const double* params, int64_t P, double
   if constexpr (NT == 3) {
     switch (k3_variant()) {
       case 421: return launch_gauss_k<3, 4, 2, 1>(pl, params, P, Mout, st, z);
+      case 422: return launch_gauss_k<3, 4, 2, 2>(pl, params, P, Mout, st, z);
+      case 4211: return launch_gauss_k<3, 4, 2, 1, kGaussMaxWarps, 1>(pl, params, P, Mout, st, z);
+      case 3211: return launch_gauss_k<3, 3, 2, 1, kGaussMaxWarps, 1>(pl, params, P, Mout, st, z);
       case 420: return launch_gauss_k<3, 4, 2, 0>(pl, params, P, Mout, st, z);
       case 231: return launch_gauss_k<3, 2, 3, 1>(pl, params, P, Mout, st, z);
       case 321: return launch_gauss_k<3, 3, 2, 1>(pl, params, P, Mout, st, z);
@@ -812,7 +868,8 @@ static int launch_gauss_nt(sas_plan* pl, const double* params, int64_t P, double
     }
   }
   constexpr int PW = gauss_pw<NT>();
-  if (k3_exp()) return launch_gauss_k<NT, PW, 2, 1>(pl, params, P, Mout, st, z);
+  if (k3_exp() == 2) return launch_gauss_k<NT, PW, 2, 2>(pl, params, P, Mout, st, z);
+  if (k3_exp() == 1) return launch_gauss_k<NT, PW, 2, 1>(pl, params, P, Mout, st, z);
   return launch_gauss_k<NT, PW, 2, 0>(pl, params, P, Mout, st, z);
 }
 

@@ -315,6 +315,33 @@ __device__ __forceinline__ double sas_exp64_t2k_fr(double a, double b, float bf,
   return __hiloint2double(hi & keep, __double2loint(res) & keep);
 }
 
+// Fast form for a CTA whose arguments all satisfy |a b| < 2.0e6 (x > -677, so
+// nothing underflows and no clamp or flush is needed; the caller checks the
+// bound per CTA).  Same arithmetic as sas_exp64_t2k_fr with fewer integer ops:
+// k from one FFMA on the magic constant (exactly rint of the FP32 product),
+// the table index straight from the float's low bits (the magic constant is a
+// multiple of 2048), and the exponent shift folded into one 3-input add.
+// a = 0 gives exactly 1.0 (k = 0, r = 2^-127).  No ridge select: the kernel
+// adds lam X[S_i] after the contraction.
+__device__ __forceinline__ double sas_exp64_t2k_fast(double a, double b, float bf, const double* __restrict__ tab_s) {
+  const int ah = max(__double2hiint(a), 0x38000000);
+  const float af = __int_as_float(ah * 8 + 0x40000000);   // (ah - 0x38000000) << 3 mod 2^32: float(a) truncated
+  const float kd32 = fmaf(af, bf, 0x1.8p23f);            // 1.5 2^23 + k, k = rint(af bf) <= 0
+  const int kdb = __float_as_int(kd32);
+  const int kb = __float_as_int(0x1.8p23f - kd32);        // bits of float(|k|), exact
+  const double kabs = __hiloint2double((kb >> 3) + 0x38000000, kb << 29);
+  const double r = fma(a, b, kabs);
+  double q = fma(r, SAS_EXP2K_A3, SAS_EXP2K_A2);
+  q = fma(q, r, SAS_EXP2K_A1);
+  q = q * r;
+  const double tv = tab_s[kdb & 2047];
+  const double res = fma(tv, q, tv);
+  // + 2^(k div 2048): (kdb >> 11) - (0x4B400000 >> 11) = k div 2048 (floor)
+  const int hi = __double2hiint(res) + ((kdb >> 11) << 20) - ((0x4B400000 >> 11) << 20);
+  return __hiloint2double(hi, __double2loint(res));
+}
+#define SAS_EXP2K_FAST_MAX 2.0e6
+
 // Host reference of the same algorithm (for the CPU accuracy test).
 double sas_exp64_host(double x);
 

@@ -108,3 +108,26 @@ def test_concurrent_callers_on_one_plan():
     for t in threads:
         t.join()
     assert not errors, errors
+
+
+def test_gauss_rows_fast_and_underflow_paths():
+    # Spread-out points: CTAs whose largest argument passes -677 (sigma = 0.5
+    # here) take the masked exponential with the ridge in the table select,
+    # the others (sigma = 2) the fast one with the ridge added after the
+    # contraction; both against the oracle, including entries that underflow.
+    prob = problems.gauss_krr(n=600, seed=3)
+    basis, sel = offline(prob)  # X and S from the original points, then spread them
+    prob.system.operator.points[...] *= 6.0  # in place (frozen dataclass)
+    plan = online.precompute_online(prob.system, basis, sel)
+    params = [0.5] * 4 + [2.0] * 4 + [0.5, 2.0, 1.3, 0.7] + [0.55] * 3
+    res = online.solve_params(plan, params)
+    assert np.all(res.status == 0)
+    op = prob.system.operator
+    fn = lambda q, rows: online_ref.gauss_rows(op.points, rows, float(q), op.ridge)
+    for k, p in enumerate(params):
+        m = online_ref.sampled_rows(fn, basis.basis, sel.indices, p)
+        t = prob.system.rhs(p, sel.indices)
+        c, _, _ = online_ref.solve_one(m, t, sel.weights)
+        floor = online_ref.ls_floor(m, t, sel.weights)
+        d = np.linalg.norm(res.coefficients[k] - c) / np.linalg.norm(c)
+        assert d <= max(1e-10, 10 * floor), (k, p, d, floor)
