@@ -1,5 +1,6 @@
 """Every least-squares kernel shape the dispatcher can pick (one warp per p,
-multi-warp register kernels, the CTA fallback), real and complex, up to the
+multi-warp register kernels, the column-owner and blocked Householder kernels
+for large real shapes, the CTA fallback), real and complex, up to the
 limits (s <= 512 real / 256 complex, r <= 63), on random weighted affine
 problems with repeated rows, against the CPU oracle."""
 import numpy as np
@@ -17,6 +18,7 @@ SHAPES = [  # (s, r, complex): every branch of launch_lsq, up to the plan limits
     (7, 6, False), (20, 8, False), (24, 11, False), (80, 20, False), (80, 23, False), (128, 11, False),
     (512, 11, False), (512, 23, False), (100, 31, False), (200, 30, False), (512, 31, False),
     (160, 40, False), (168, 47, False), (200, 50, False), (256, 55, False), (256, 63, False),
+    (45, 40, False), (150, 41, False), (130, 44, False), (224, 49, False), (190, 52, False),
     (20, 8, True), (120, 8, True), (256, 11, True), (100, 31, True), (256, 40, True), (128, 63, True),
 ]
 
@@ -71,3 +73,30 @@ def test_limits_rejected():
         sel64 = RowSelector(indices=np.arange(70) % system.n, n=system.n)
         with pytest.raises(ValueError):
             online.precompute_online(system, wide, sel64)
+
+
+@pytest.mark.parametrize("s,r", [(160, 40), (200, 50), (256, 55)])
+def test_large_shapes_rank_deficient_and_nonfinite(s, r):
+    # the column-owner (160x40, 200x50, 256x55) kernel reports the reference's
+    # errors: a repeated basis column is rank-deficient (status 1, the repeated
+    # column named, RankDeficiencyError from solve_batch), a NaN in a sampled
+    # row is non-finite (status 2, ValueError)
+    from paper_2510_04825_b200.errors import RankDeficiencyError
+    system, basis, sel, params = _problem(s, r, False, seed=7)
+    q = basis.basis.copy()
+    q[:, r - 2] = q[:, 3]
+    dup = SnapshotBasis(points=(), raw=q, basis=q, singular_values=np.ones(r))
+    plan = online.precompute_online(system, dup, sel)
+    res = online.solve_params(plan, params)
+    assert np.all(res.status == 1) and np.all(res.bad_column == r - 2), (res.status, res.bad_column)
+    assert np.all(np.isnan(res.coefficients))
+    with pytest.raises(RankDeficiencyError):
+        online.solve_batch(plan, params[:2])
+    q = basis.basis.copy()
+    q[sel.indices[s // 2], r // 2] = np.nan
+    bad = SnapshotBasis(points=(), raw=q, basis=q, singular_values=np.ones(r))
+    plan = online.precompute_online(system, bad, sel)
+    res = online.solve_params(plan, params)
+    assert np.all(res.status == 2)
+    with pytest.raises(ValueError, match="non-finite"):
+        online.solve_batch(plan, params[:2])
