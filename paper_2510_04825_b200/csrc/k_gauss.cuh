@@ -163,17 +163,23 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                : "memory");
 }
 
+// Shared memory: the stage ring, the negated exp table (2048) and the negated
+// diagonal entries -(1 + lam_u), then the mbarriers.
+constexpr int kGaussTabDoubles = 2048 + 16;
 template <int NT>
 __host__ __device__ constexpr size_t gauss3_smem_bytes(int rows_cta) {
-  return (size_t)kG3Stages * (rows_cta / 8 + NT) * kG3KS * 32 * sizeof(double) + (2048 + 8) * sizeof(double) +
+  return (size_t)kG3Stages * (rows_cta / 8 + NT) * kG3KS * 32 * sizeof(double) + kGaussTabDoubles * sizeof(double) +
          2 * kG3Stages * sizeof(uint64_t);
 }
 
-// EXPV selects the exponential: 0 = sas_exp64_t2k_ridge (7 FP64-pipe ops),
-// 1 = sas_exp64_t2k_fr (5; FP32/integer range reduction, the default).
+// Exponentials: CTAs whose largest argument stays above -677 (dmax = max D in
+// table units, times the CTA's largest 1/(2 sigma^2)) use sas_exp64_t2k_fast
+// and add the kernel ridge after the contraction (M += lam X[S_i]); the others
+// use the masked sas_exp64_t2k_fr with the ridge folded into the diagonal
+// entry (the reference's exp(-0) + lam, _kernels.py:49).
 // Split-K: grid.z splits the n chunks into gridDim.z contiguous ranges whose
 // partial products go to Mout + z * msplit; K4 sums them in z order.
-template <int NT, int PW, int MINB, int EXPV, int MAXW, int SWP>
+template <int NT, int PW, int MINB, int MAXW>
 __global__ void __launch_bounds__(32 * MAXW, MINB)
 k_gauss_rows(const double* __restrict__ Df, const double* __restrict__ Xf, const int64_t* __restrict__ S,
              const double* __restrict__ params, int dp, int64_t P, int s, int64_t nchunks, int r, double ridge,
@@ -184,8 +190,9 @@ k_gauss_rows(const double* __restrict__ Df, const double* __restrict__ Xf, const
   const int rows_cta = nrg * 8;
   const int row0 = blockIdx.y * rows_cta;
   const int stage_d = (nrg + NT) * kG3KS * 32;  // doubles per stage
-  double* tab_s = gsm + (size_t)kG3Stages * stage_d;
-  uint64_t* full = reinterpret_cast<uint64_t*>(tab_s + 2048 + 8);
+  double* ring = gsm;
+  double* tabn = gsm + (size_t)kG3Stages * stage_d;  // -2^(j/2048), then -(1 + lam_u)
+  uint64_t* full = reinterpret_cast<uint64_t*>(tabn + kGaussTabDoubles);
   uint64_t* empty = full + kG3Stages;
   const unsigned dbytes = (unsigned)(nrg * kG3KS * 32 * sizeof(double));
   const unsigned xbytes = (unsigned)(NT * kG3KS * 32 * sizeof(double));
@@ -198,7 +205,7 @@ k_gauss_rows(const double* __restrict__ Df, const double* __restrict__ Xf, const
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  for (int j = threadIdx.x; j < 2048; j += blockDim.x) tab_s[j] = g_exp2_tab2048[j];
+  for (int j = threadIdx.x; j < 2048; j += blockDim.x) tabn[j] = -g_exp2_tab2048[j];
   __syncthreads();
 
   const int64_t c0 = nchunks * blockIdx.z / gridDim.z, nloc = nchunks * (blockIdx.z + 1) / gridDim.z - c0;
@@ -206,7 +213,7 @@ k_gauss_rows(const double* __restrict__ Df, const double* __restrict__ Xf, const
   auto issue = [&](int64_t j) {  // local chunk j = chunk c0 + j into slot j mod stages
     const int b = (int)(j % kG3Stages);
     if (j >= kG3Stages) mbar_wait(&empty[b], (unsigned)(((j / kG3Stages) - 1) & 1));
-    double* dst = gsm + (size_t)b * stage_d;
+    double* dst = ring + (size_t)b * stage_d;
     const int64_t ch = c0 + j;
     mbar_expect_tx(&full[b], dbytes + xbytes);
     bulk_g2s(dst, dsrc + ch * (int64_t)nrg * kG3KS * 32, dbytes, &full[b]);
@@ -220,30 +227,24 @@ k_gauss_rows(const double* __restrict__ Df, const double* __restrict__ Xf, const
   const int64_t pbase = (int64_t)blockIdx.x * PW;
   double ninv[PW];
   float ninvf[PW];
+  double bmax = 0.0;
 #pragma unroll
   for (int u = 0; u < PW; ++u) {
     const int64_t p = pbase + u;
     const double sg = (p < P) ? params[p * dp + dp - 1] : 1.0;
     ninv[u] = -(1.0 / (2.0 * sg * sg));  // reference: inv = 1.0 / (2.0 * sigma * sigma)
     ninvf[u] = (float)ninv[u];
+    bmax = fmax(bmax, -ninv[u]);
   }
-  if (threadIdx.x < PW) {
-    const int64_t p = pbase + threadIdx.x;
-    const double lam = (dp == 2) ? ((p < P) ? params[p * 2] : 0.0) : ridge;
-    tab_s[2048 + threadIdx.x] = 1.0 + lam;  // the reference's exp(-0) + lam (_kernels.py:49)
-  }
+  auto lam_of = [&](int u) {
+    const int64_t p = pbase + u;
+    return (dp == 2) ? ((p < P) ? params[p * 2] : 0.0) : ridge;
+  };
+  if (threadIdx.x < PW) tabn[2048 + threadIdx.x] = -(1.0 + lam_of(threadIdx.x));
   __syncthreads();
   const int grow = row0 + warp * 8 + (lane >> 2);
   const int64_t srow = (grow < s) ? S[grow] : -1;
-  // EXPV 2: CTAs whose largest argument stays above -677 (dmax = max D in table
-  // units) take the fast exponential and add the ridge after the contraction.
-  bool fast = false;
-  if (EXPV == 2) {
-    double bmax = 0.0;
-#pragma unroll
-    for (int u = 0; u < PW; ++u) bmax = fmax(bmax, -ninv[u]);
-    fast = dmax * bmax < SAS_EXP2K_FAST_MAX;
-  }
+  const bool fast = dmax * bmax < SAS_EXP2K_FAST_MAX;
 
   double acc[PW][NT][2];
 #pragma unroll
@@ -251,17 +252,13 @@ k_gauss_rows(const double* __restrict__ Df, const double* __restrict__ Xf, const
 #pragma unroll
     for (int t = 0; t < NT; ++t) acc[u][t][0] = acc[u][t][1] = 0.0;
 
-  auto expf = [&](double dv, int u, bool diag) {
-    return EXPV ? sas_exp64_t2k_fr(dv, ninv[u], ninvf[u], tab_s, diag ? 2048 + u : -1)
-                : sas_exp64_t2k_ridge(dv, ninv[u], tab_s, diag ? 2048 + u : -1);
-  };
-  if (EXPV == 2 && fast) {
+  if (fast) {
     for (int64_t j = 0; j < nloc; ++j) {
       if (threadIdx.x == 0 && j + kG3Stages - 1 < nloc) issue(j + kG3Stages - 1);
       const int b = (int)(j % kG3Stages);
       mbar_wait(&full[b], (unsigned)((j / kG3Stages) & 1));
-      const double* dsb = gsm + (size_t)b * stage_d + warp * kG3KS * 32 + lane;
-      const double* xsb = gsm + (size_t)b * stage_d + nrg * kG3KS * 32 + lane;
+      const double* dsb = ring + (size_t)b * stage_d + warp * kG3KS * 32 + lane;
+      const double* xsb = ring + (size_t)b * stage_d + nrg * kG3KS * 32 + lane;
 #pragma unroll kK3Unroll
       for (int ks = 0; ks < kG3KS; ++ks) {
         const double dv = dsb[ks * 32];
@@ -270,7 +267,7 @@ k_gauss_rows(const double* __restrict__ Df, const double* __restrict__ Xf, const
         for (int t = 0; t < NT; ++t) bf[t] = xsb[(t * kG3KS + ks) * 32];
 #pragma unroll
         for (int u = 0; u < PW; ++u) {
-          const double e = sas_exp64_t2k_fast(dv, ninv[u], ninvf[u], tab_s);
+          const double e = sas_exp64_t2k_fast(dv, ninv[u], ninvf[u], tabn);
 #pragma unroll
           for (int t = 0; t < NT; ++t) dmma884(acc[u][t][0], acc[u][t][1], e, bf[t]);
         }
@@ -283,7 +280,7 @@ k_gauss_rows(const double* __restrict__ Df, const double* __restrict__ Xf, const
       const double* xrow = X + srow * (int64_t)r;
 #pragma unroll
       for (int u = 0; u < PW; ++u) {
-        const double lam = (dp == 2) ? ((pbase + u < P) ? params[(pbase + u) * 2] : 0.0) : ridge;
+        const double lam = lam_of(u);
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
           const int c0c = t * 8 + 2 * (lane & 3);
@@ -292,77 +289,27 @@ k_gauss_rows(const double* __restrict__ Df, const double* __restrict__ Xf, const
         }
       }
     }
-  } else if constexpr (SWP) {
-    // Software-pipelined: the exponentials of k-step kk+1 are evaluated while the
-    // DMMAs of k-step kk (on values computed one step earlier) issue, so no DMMA
-    // waits on a just-computed exp chain.  The last k-step of a chunk reads the
-    // next chunk's first D fragment (two chunks resident, then the first is released).
-    double ecur[PW];
-    if (nloc > 0) {
-      mbar_wait(&full[0], 0u);
-      const double dv = gsm[warp * kG3KS * 32 + lane];
-      const int64_t l0 = c0 * kGaussKC;
-      const bool diag = srow == l0 + (lane & 3);
-#pragma unroll
-      for (int u = 0; u < PW; ++u) ecur[u] = expf(dv, u, diag);
-    }
-    for (int64_t j = 0; j < nloc; ++j) {
-      if (threadIdx.x == 0 && j + kG3Stages - 1 < nloc) issue(j + kG3Stages - 1);
-      const int b = (int)(j % kG3Stages);
-      const double* dsb = gsm + (size_t)b * stage_d + warp * kG3KS * 32 + lane;
-      const double* xsb = gsm + (size_t)b * stage_d + nrg * kG3KS * 32 + lane;
-      const int64_t l0 = (c0 + j) * kGaussKC;
-      const int dcol = (srow >= l0 && srow < l0 + kGaussKC) ? (int)(srow - l0) : -1;
-#pragma unroll
-      for (int ks = 0; ks < kG3KS; ++ks) {
-        double enext[PW];
-        if (ks + 1 < kG3KS) {
-          const double dv = dsb[(ks + 1) * 32];
-          const bool diag = (4 * (ks + 1) + (lane & 3)) == dcol;
-#pragma unroll
-          for (int u = 0; u < PW; ++u) enext[u] = expf(dv, u, diag);
-        } else if (j + 1 < nloc) {
-          const int bn = (int)((j + 1) % kG3Stages);
-          mbar_wait(&full[bn], (unsigned)(((j + 1) / kG3Stages) & 1));
-          const double dv = gsm[(size_t)bn * stage_d + warp * kG3KS * 32 + lane];
-          const bool diag = srow == l0 + kGaussKC + (lane & 3);
-#pragma unroll
-          for (int u = 0; u < PW; ++u) enext[u] = expf(dv, u, diag);
-        }
-        double bf[NT];
-#pragma unroll
-        for (int t = 0; t < NT; ++t) bf[t] = xsb[(t * kG3KS + ks) * 32];
-#pragma unroll
-        for (int u = 0; u < PW; ++u)
-#pragma unroll
-          for (int t = 0; t < NT; ++t) dmma884(acc[u][t][0], acc[u][t][1], ecur[u], bf[t]);
-#pragma unroll
-        for (int u = 0; u < PW; ++u) ecur[u] = enext[u];
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[b]);
-    }
   } else {
     for (int64_t j = 0; j < nloc; ++j) {
       if (threadIdx.x == 0 && j + kG3Stages - 1 < nloc) issue(j + kG3Stages - 1);
       const int b = (int)(j % kG3Stages);
       mbar_wait(&full[b], (unsigned)((j / kG3Stages) & 1));
       const int64_t ch = c0 + j;
-      const double* dsb = gsm + (size_t)b * stage_d + warp * kG3KS * 32 + lane;
-      const double* xsb = gsm + (size_t)b * stage_d + nrg * kG3KS * 32 + lane;
+      const double* dsb = ring + (size_t)b * stage_d + warp * kG3KS * 32 + lane;
+      const double* xsb = ring + (size_t)b * stage_d + nrg * kG3KS * 32 + lane;
       const int64_t l0 = ch * kGaussKC;
       const int dcol = (srow >= l0 && srow < l0 + kGaussKC) ? (int)(srow - l0) : -1;
-  #pragma unroll kK3Unroll
+#pragma unroll kK3Unroll
       for (int ks = 0; ks < kG3KS; ++ks) {
         const double dv = dsb[ks * 32];
         double bf[NT];
-  #pragma unroll
+#pragma unroll
         for (int t = 0; t < NT; ++t) bf[t] = xsb[(t * kG3KS + ks) * 32];
         const bool diag = (4 * ks + (lane & 3)) == dcol;
-  #pragma unroll
+#pragma unroll
         for (int u = 0; u < PW; ++u) {
-          const double e = expf(dv, u, diag);
-  #pragma unroll
+          const double e = sas_exp64_t2k_fr(dv, ninv[u], ninvf[u], tabn, diag ? 2048 + u : -1);
+#pragma unroll
           for (int t = 0; t < NT; ++t) dmma884(acc[u][t][0], acc[u][t][1], e, bf[t]);
         }
       }

@@ -64,28 +64,6 @@ void sas_set_error(const char* fmt, ...) {
     }                               \
   } while (0)
 
-// Host mirror of the K3 exponential (sas_exp64_t2k_ridge(x, 2048/ln2)), bit for bit.
-double sas_exp64_host(double x) {
-  const double kd = fma(x, SAS_INVLN2X2K, SAS_EXP_MAGIC);
-  int64_t bits;
-  memcpy(&bits, &kd, 8);
-  const int ki = (int)(uint32_t)(bits & 0xffffffffu);
-  volatile double kfv = kd - SAS_EXP_MAGIC;
-  const double kf = kfv;
-  const double r = fma(x, SAS_INVLN2X2K, -kf);
-  double q = fma(r, SAS_EXP2K_A3, SAS_EXP2K_A2);
-  q = fma(q, r, SAS_EXP2K_A1);
-  volatile double qv = q * r;
-  q = qv;
-  const double tab = h_exp2_tab2048[ki & 2047];
-  double res = fma(tab, q, tab);
-  int64_t rb;
-  memcpy(&rb, &res, 8);
-  rb += (int64_t)(ki >> 11) << 52;
-  memcpy(&res, &rb, 8);
-  return (ki >= SAS_EXP2K_KMIN) ? res : 0.0;
-}
-
 // Host mirror of sas_exp64_t2k_fr (a >= 0, b < 0), bit for bit.
 static double sas_exp64_fr_host(double a, double b) {
   const float bf = (float)b;
@@ -159,7 +137,6 @@ static double sas_exp64_fast_host(double a, double b) {
   return res;
 }
 
-static int k3_exp();
 
 // ---------------------------------------------------------------------------
 struct sas_plan {
@@ -337,28 +314,28 @@ __global__ void k_stencil_gather(const double* __restrict__ X, int r, const int6
 
 extern "C" const char* sas_last_error(void) { return g_err.c_str(); }
 extern "C" const char* sas_version(void) { return "sas 0.1.0 (sm_100a)"; }
-// The debug exponential is the one K3 uses (SAS_K3_EXP).
-extern "C" double sas_debug_exp64_host(double x) {
-  if (k3_exp() == 2 && -x * SAS_INVLN2X2K < SAS_EXP2K_FAST_MAX)  // the CTA-uniform K3 test, per value
-    return sas_exp64_fast_host(-x * SAS_INVLN2X2K, -1.0);
-  return k3_exp() ? sas_exp64_fr_host(-x, -SAS_INVLN2X2K) : sas_exp64_host(x);
+// The debug exponential is the one K3 uses: the fast form where the CTA test
+// (|x| 2048/ln2 < SAS_EXP2K_FAST_MAX) passes, the masked form elsewhere.
+double sas_exp64_host(double x) {
+  if (-x * SAS_INVLN2X2K < SAS_EXP2K_FAST_MAX) return sas_exp64_fast_host(-x * SAS_INVLN2X2K, -1.0);
+  return sas_exp64_fr_host(-x, -SAS_INVLN2X2K);
 }
+extern "C" double sas_debug_exp64_host(double x) { return sas_exp64_host(x); }
 
-__global__ void k_debug_exp64(const double* x, double* y, int64_t n, int expv) {
-  __shared__ double tab_s[2048];
-  for (int j = threadIdx.x; j < 2048; j += blockDim.x) tab_s[j] = g_exp2_tab2048[j];
+__global__ void k_debug_exp64(const double* x, double* y, int64_t n) {
+  __shared__ double tabn[2048];
+  for (int j = threadIdx.x; j < 2048; j += blockDim.x) tabn[j] = -g_exp2_tab2048[j];
   __syncthreads();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    y[i] = (expv == 2 && -x[i] * SAS_INVLN2X2K < SAS_EXP2K_FAST_MAX)
-               ? sas_exp64_t2k_fast(-x[i] * SAS_INVLN2X2K, -1.0, -1.0f, tab_s)
-               : expv ? sas_exp64_t2k_fr(-x[i], -SAS_INVLN2X2K, (float)-SAS_INVLN2X2K, tab_s, -1)
-                      : sas_exp64_t2k_ridge(x[i], SAS_INVLN2X2K, tab_s, -1);
+    y[i] = (-x[i] * SAS_INVLN2X2K < SAS_EXP2K_FAST_MAX)
+               ? sas_exp64_t2k_fast(-x[i] * SAS_INVLN2X2K, -1.0, -1.0f, tabn)
+               : sas_exp64_t2k_fr(-x[i], -SAS_INVLN2X2K, (float)-SAS_INVLN2X2K, tabn, -1);
 }
 
 // Device evaluation of the K3 exponential (on t = x * 2048/ln2) for accuracy tests; device pointers.
 extern "C" int sas_debug_exp64(const double* x, double* y, int64_t n, void* stream) {
   if (n <= 0) return SAS_OK;
-  k_debug_exp64<<<256, 256, 0, (cudaStream_t)stream>>>(x, y, n, k3_exp());
+  k_debug_exp64<<<256, 256, 0, (cudaStream_t)stream>>>(x, y, n);
   SAS_CUDA_CHECK(cudaGetLastError());
   return SAS_OK;
 }
@@ -781,10 +758,9 @@ static int launch_lsq(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t s
 }
 
 // K3 launch: PW (parameter values per CTA) from the accumulator budget
-// (gauss_pw), 2 CTAs/SM, the FP32/integer-reduction exponential, split-K chosen
-// against the wave count.  Tuning: SAS_K3_VARIANT=<pw>,<minb>[,<expv>] for
-// 17 <= r <= 24 (NT == 3), SAS_K3_EXP=0|1|2 (7-op, FP32-reduction, fast with the
-// ridge added after the contraction), SAS_K3_KSPLIT, SAS_K3_MAXW.
+// (gauss_pw), 2 CTAs/SM, split-K chosen against the wave count.  Tuning:
+// SAS_K3_VARIANT=<pw>,<minb> for 17 <= r <= 24 (NT == 3), SAS_K3_KSPLIT,
+// SAS_K3_MAXW.
 // Split-K factor: the smallest z in 1..kGaussMaxSplit minimising the wave
 // count ceil(ctas z / slots) / z (a partial last wave of whole-n CTAs costs up
 // to a full wave); SAS_K3_KSPLIT forces it.
@@ -801,7 +777,7 @@ static int gauss_ksplit(int64_t ctas, int64_t slots, int64_t nchunks) {
   return best;
 }
 
-template <int NT, int PW, int MINB, int EXPV, int MAXW = kGaussMaxWarps, int SWP = 0>
+template <int NT, int PW, int MINB, int MAXW = kGaussMaxWarps>
 static int launch_gauss_k(sas_plan* pl, const double* params, int64_t P, double* Mout, cudaStream_t st,
                           int* ksplit) {
   int gy, rows_cta;
@@ -812,7 +788,7 @@ static int launch_gauss_k(sas_plan* pl, const double* params, int64_t P, double*
     return SAS_ERR_ARG;
   }
   const size_t smem = gauss3_smem_bytes<NT>(rows_cta);
-  auto kern = k_gauss_rows<NT, PW, MINB, EXPV, MAXW, SWP>;
+  auto kern = k_gauss_rows<NT, PW, MINB, MAXW>;
   SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   SAS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * nw, smem));
@@ -829,25 +805,14 @@ static int launch_gauss_k(sas_plan* pl, const double* params, int64_t P, double*
   return SAS_OK;
 }
 
-#ifndef SAS_K3_EXP_DEFAULT
-#define SAS_K3_EXP_DEFAULT 2
-#endif
-static int k3_exp() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SAS_K3_EXP");
-    v = e ? std::max(0, std::min(2, atoi(e))) : SAS_K3_EXP_DEFAULT;
-  }
-  return v;
-}
 static int k3_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("SAS_K3_VARIANT");
     v = 0;
     if (e) {
-      int pw = 0, mb = 0, ex = 1, sw = 0;
-      if (sscanf(e, "%d,%d,%d,%d", &pw, &mb, &ex, &sw) >= 2) v = (pw * 100 + mb * 10 + ex) * (sw ? 10 : 1) + (sw ? 1 : 0);
+      int pw = 0, mb = 0;
+      if (sscanf(e, "%d,%d", &pw, &mb) == 2) v = pw * 10 + mb;
     }
   }
   return v;
@@ -857,20 +822,13 @@ template <int NT>
 static int launch_gauss_nt(sas_plan* pl, const double* params, int64_t P, double* Mout, cudaStream_t st, int* z) {
   if constexpr (NT == 3) {
     switch (k3_variant()) {
-      case 421: return launch_gauss_k<3, 4, 2, 1>(pl, params, P, Mout, st, z);
-      case 422: return launch_gauss_k<3, 4, 2, 2>(pl, params, P, Mout, st, z);
-      case 4211: return launch_gauss_k<3, 4, 2, 1, kGaussMaxWarps, 1>(pl, params, P, Mout, st, z);
-      case 3211: return launch_gauss_k<3, 3, 2, 1, kGaussMaxWarps, 1>(pl, params, P, Mout, st, z);
-      case 420: return launch_gauss_k<3, 4, 2, 0>(pl, params, P, Mout, st, z);
-      case 231: return launch_gauss_k<3, 2, 3, 1>(pl, params, P, Mout, st, z);
-      case 321: return launch_gauss_k<3, 3, 2, 1>(pl, params, P, Mout, st, z);
+      case 42: return launch_gauss_k<3, 4, 2>(pl, params, P, Mout, st, z);
+      case 23: return launch_gauss_k<3, 2, 3>(pl, params, P, Mout, st, z);
+      case 32: return launch_gauss_k<3, 3, 2>(pl, params, P, Mout, st, z);
       default: break;
     }
   }
-  constexpr int PW = gauss_pw<NT>();
-  if (k3_exp() == 2) return launch_gauss_k<NT, PW, 2, 2>(pl, params, P, Mout, st, z);
-  if (k3_exp() == 1) return launch_gauss_k<NT, PW, 2, 1>(pl, params, P, Mout, st, z);
-  return launch_gauss_k<NT, PW, 2, 0>(pl, params, P, Mout, st, z);
+  return launch_gauss_k<NT, gauss_pw<NT>(), 2>(pl, params, P, Mout, st, z);
 }
 
 static int launch_gauss(sas_plan* pl, const double* params, int64_t P, double* Mout, cudaStream_t st, int* z) {

@@ -254,48 +254,27 @@ __device__ __forceinline__ double sas_exp64_t2k(double x, const double* __restri
   return __hiloint2double(hi & keep, __double2loint(res) & keep);
 }
 
-// K3 exponential in "table units": e^(a*b) for a = D' (kernel-row distance
-// pre-scaled by 2048/ln2 at plan time) and b = -inv = -1/(2p^2), i.e. the
-// argument a*b is x * 2048/ln2.  k = rint(a*b) and r = a*b - k both come from
-// one FMA on the exact product (|r| <= 1/2, one rounding), so no rounded copy
-// of the argument is formed; e^x = 2^(k/2048) 2^(r/2048), 2^(r/2048) - 1 =
-// r (a1 + r (a2 + r a3)) with a_i = (ln2/2048)^i / i! (truncation <= 3.5e-17).
-// 7 FP64-pipe ops.  The plan-time rounding of D' gives a relative error
-// ~|x| eps/2, the same as the rounding of x = -D*inv in the reference.  The kernel-row
-// ridge is folded in: on the diagonal entry (l == S_i) D = 0, so r = +-0,
-// q = +-0 and the result is the selected table value; selecting (1 + ridge)
-// gives exactly the reference's exp(-0) + lam.
 #define SAS_EXP2K_A1 0x1.62e42fefa39efp-12
 #define SAS_EXP2K_A2 0x1.ebfbdff82c58fp-25
 #define SAS_EXP2K_A3 0x1.c6b08d704a0c0p-38
 
-__device__ __forceinline__ double sas_exp64_t2k_ridge(double a, double b, const double* __restrict__ tab_s,
-                                                      int ridx) {
-  const double kd = fma(a, b, SAS_EXP_MAGIC);
-  const int ki = __double2loint(kd);
-  const double kf = __dsub_rn(kd, SAS_EXP_MAGIC);
-  const double r = fma(a, b, -kf);
-  double q = fma(r, SAS_EXP2K_A3, SAS_EXP2K_A2);
-  q = fma(q, r, SAS_EXP2K_A1);
-  q = q * r;
-  const double tv = tab_s[ridx >= 0 ? ridx : (ki & 2047)];
-  const double res = fma(tv, q, tv);
-  const int hi = __double2hiint(res) + ((ki >> 11) << 20);
-  const int keep = (ki >= SAS_EXP2K_KMIN) ? -1 : 0;
-  return __hiloint2double(hi & keep, __double2loint(res) & keep);
-}
-
-// Same exponential with the range reduction moved off the FP64 pipe (5
-// FP64-pipe ops instead of 7).  Requires a >= 0 and b < 0 (the kernel rows'
-// argument is always <= 0); bf = (float)b.
-//   k = rint(a*b) from an FP32 product of truncated copies (integer bit ops give
-//   float(a); |k - a*b| <= 1/2 + 2^-22 |a*b|, so |r| <= 0.52 with the clamp below
-//   keeping |k| < 2^22), |k| as an exact double built from the float's bits, then
-//   r = a*b + |k| in one FMA on the exact product, as above.  The polynomial
-//   truncation at |r| = 0.52 is 4e-17.  k = 0 yields |k| = 2^-127 instead of 0,
-//   which perturbs r by 2^-127 (below half an ulp of any nonzero r) and leaves the
-//   diagonal entry (a = 0) exactly the selected table value.
-__device__ __forceinline__ double sas_exp64_t2k_fr(double a, double b, float bf, const double* __restrict__ tab_s,
+// K3 exponentials in "table units": e^(a*b) for a = D' >= 0 (kernel-row
+// distance pre-scaled by 2048/ln2 at plan time) and b = -1/(2 p^2) < 0, with
+// bf = (float)b.  tabn holds the table NEGATED (-2^(j/2048)): the final
+// fma then yields -t(1+q) and the sign is cleared by the same integer add
+// that applies 2^(k div 2048) (see below), saving an instruction per value.
+//
+// sas_exp64_t2k_fr: k = rint(a*b) from an FP32 product of truncated copies
+// (integer bit ops give float(a)); |k - a*b| <= 1/2 + 2^-22 |a*b|, so with the
+// clamp below (|k| < 2^22) the reduced argument r = a*b + |k| (one FMA on the
+// exact product, |k| rebuilt as an exact double from the float's bits) has
+// |r| <= 0.52, where the degree-3 polynomial's truncation is 4e-17.
+// 2^(r/2048) - 1 = r (a1 + r (a2 + r a3)), a_i = (ln2/2048)^i / i!.  5 FP64-pipe
+// ops.  k = 0 yields |k| = 2^-127 instead of 0, which perturbs r by 2^-127
+// (below half an ulp of any nonzero r) and leaves a = 0 exactly the selected
+// table value.  k < -2093055 (x < -708.39) flushes to +0.  ridx >= 0 selects
+// tabn[ridx] instead of the table (the kernel-row ridge on the diagonal).
+__device__ __forceinline__ double sas_exp64_t2k_fr(double a, double b, float bf, const double* __restrict__ tabn,
                                                    int ridx) {
   const int ah = max(__double2hiint(a), 0x38000000);
   const float af = __int_as_float((ah - 0x38000000) << 3);  // float(a) truncated; a < 2^-126 -> 0
@@ -308,22 +287,23 @@ __device__ __forceinline__ double sas_exp64_t2k_fr(double a, double b, float bf,
   double q = fma(r, SAS_EXP2K_A3, SAS_EXP2K_A2);
   q = fma(q, r, SAS_EXP2K_A1);
   q = q * r;
-  const double tv = tab_s[ridx >= 0 ? ridx : (ki & 2047)];
-  const double res = fma(tv, q, tv);
-  const int hi = __double2hiint(res) + ((ki >> 11) << 20);
+  const double tv = tabn[ridx >= 0 ? ridx : (ki & 2047)];
+  const double res = fma(tv, q, tv);  // -t (1 + q)
+  const int hi = (__double2hiint(res) + ((ki >> 11) << 20)) ^ (int)0x80000000;
   const int keep = (ki >= SAS_EXP2K_KMIN) ? -1 : 0;
   return __hiloint2double(hi & keep, __double2loint(res) & keep);
 }
 
-// Fast form for a CTA whose arguments all satisfy |a b| < 2.0e6 (x > -677, so
-// nothing underflows and no clamp or flush is needed; the caller checks the
-// bound per CTA).  Same arithmetic as sas_exp64_t2k_fr with fewer integer ops:
-// k from one FFMA on the magic constant (exactly rint of the FP32 product),
-// the table index straight from the float's low bits (the magic constant is a
-// multiple of 2048), and the exponent shift folded into one 3-input add.
-// a = 0 gives exactly 1.0 (k = 0, r = 2^-127).  No ridge select: the kernel
-// adds lam X[S_i] after the contraction.
-__device__ __forceinline__ double sas_exp64_t2k_fast(double a, double b, float bf, const double* __restrict__ tab_s) {
+// sas_exp64_t2k_fast: the same arithmetic for a CTA whose arguments all satisfy
+// |a b| < 2.0e6 (x > -677: nothing underflows, no clamp or flush; the caller
+// checks the bound per CTA), with fewer integer instructions: k from one FFMA
+// on the magic constant (exactly rint of the FP32 product), the table index
+// straight from the float's low bits (the magic constant is a multiple of
+// 2048), and sign + 2^(k div 2048) in one add: the float bits kdb = 0x4B400000
+// + k give (kdb >> 11) << 20 = 0x80000000 + (k div 2048) << 20 (mod 2^32), and
+// the 0x80000000 clears the sign of -t(1+q).  a = 0 gives exactly 1.0.  No
+// ridge select: K3 adds lam X[S_i] after the contraction.
+__device__ __forceinline__ double sas_exp64_t2k_fast(double a, double b, float bf, const double* __restrict__ tabn) {
   const int ah = max(__double2hiint(a), 0x38000000);
   const float af = __int_as_float(ah * 8 + 0x40000000);   // (ah - 0x38000000) << 3 mod 2^32: float(a) truncated
   const float kd32 = fmaf(af, bf, 0x1.8p23f);            // 1.5 2^23 + k, k = rint(af bf) <= 0
@@ -334,10 +314,9 @@ __device__ __forceinline__ double sas_exp64_t2k_fast(double a, double b, float b
   double q = fma(r, SAS_EXP2K_A3, SAS_EXP2K_A2);
   q = fma(q, r, SAS_EXP2K_A1);
   q = q * r;
-  const double tv = tab_s[kdb & 2047];
-  const double res = fma(tv, q, tv);
-  // + 2^(k div 2048): (kdb >> 11) - (0x4B400000 >> 11) = k div 2048 (floor)
-  const int hi = __double2hiint(res) + ((kdb >> 11) << 20) - ((0x4B400000 >> 11) << 20);
+  const double tv = tabn[kdb & 2047];
+  const double res = fma(tv, q, tv);  // -t (1 + q)
+  const int hi = __double2hiint(res) + ((kdb >> 11) << 20);
   return __hiloint2double(hi, __double2loint(res));
 }
 #define SAS_EXP2K_FAST_MAX 2.0e6

@@ -1,6 +1,6 @@
 """Time K3 variants on the config-2 workload (one process per variant because
 the variant is read once from the environment).  A variant is
-"pw,minb,expv,swp[,maxw[,ksplit]]" (SAS_K3_VARIANT; maxw -> SAS_K3_MAXW, the
+"pw,minb[,maxw[,ksplit]]" (SAS_K3_VARIANT; maxw -> SAS_K3_MAXW, the
 warps per CTA row block; ksplit -> SAS_K3_KSPLIT, "a" = automatic).  Each line also reports the worst coefficient difference
 against the CPU oracle on 4 bandwidths.   Usage: VARIANTS="..." python tools/tune_k3.py"""
 import os
@@ -9,7 +9,7 @@ import sys
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
-VARIANTS = os.environ.get("VARIANTS", "4,2,1,0,10,a 4,2,1,1,10,a 3,2,1,1,10,a").split()
+VARIANTS = os.environ.get("VARIANTS", "4,2,10,a 4,2,10,1 3,2,10,a").split()
 
 CHILD = r'''
 import json, sys, time
@@ -47,11 +47,11 @@ print(json.dumps({"k3_ms": min(k3), "k4_ms": min(k4), "tflops": 2*80*20000*20*40
 
 for v in VARIANTS:
     f = v.split(",")
-    env = dict(os.environ, SAS_K3_VARIANT=",".join(f[:4]))
-    if len(f) >= 5:
-        env["SAS_K3_MAXW"] = f[4]
-    if len(f) >= 6 and f[5] != "a":
-        env["SAS_K3_KSPLIT"] = f[5]
+    env = dict(os.environ, SAS_K3_VARIANT=",".join(f[:2]))
+    if len(f) >= 3:
+        env["SAS_K3_MAXW"] = f[2]
+    if len(f) >= 4 and f[3] != "a":
+        env["SAS_K3_KSPLIT"] = f[3]
     r = subprocess.run([sys.executable, "-c", CHILD, str(ROOT)], env=env, capture_output=True, text=True)
     line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-800:]
     print(v, line, flush=True)
