@@ -3,8 +3,9 @@
 //
 // K5 (real): x^T = X C^T as a DMMA GEMM (mma.sync.m8n8k4.f64): A = X tile
 // (64 nodes x r, staged in shared memory), B = C^T tile (r x 64 parameters),
-// one warp per 8 nodes x 64 parameters, K = r padded to 4.  The residual then
-// runs on the materialised x in chunks of parameters (k_resid_*_x).
+// one warp per 8 nodes x 64 parameters, K = r padded to 4.  The stencil
+// residual then runs on the materialised x in chunks of 64 parameters, stored
+// in 16-parameter blocks (k_resid_stencil_b16).
 #pragma once
 #include "sas_common.cuh"
 
@@ -25,13 +26,14 @@ __host__ __device__ inline int lift_ld(int r) {
   return kp;
 }
 
-// grid = (ceil(n/64), ceil(P/64)); block 256.  Output x[p*n + i] (NODE_MAJOR =
-// false, the lift() layout) or x[i*ldx + p] (NODE_MAJOR = true, the residual
-// checker's layout: a node's values for consecutive parameters share a line).
-template <bool NODE_MAJOR>
+// grid = (ceil(n/64), ceil(P/64)); block 256.  Output x[p*n + i] (BLK16 =
+// false, the lift() layout) or x[((p / 16) n + i) 16 + p mod 16] (BLK16 = true,
+// the residual checker's layout: a node's values for 16 consecutive parameters
+// fill one aligned 128-byte line).
+template <bool BLK16>
 __global__ void __launch_bounds__(256) k_lift_dmma(const double* __restrict__ X, int64_t n, int r,
                                                    const double* __restrict__ C, int64_t P,
-                                                   double* __restrict__ x, int64_t ldx) {
+                                                   double* __restrict__ x) {
   extern __shared__ __align__(16) double lsm[];
   const int ld = lift_ld(r);
   const int kp = ((r + 3) / 4) * 4;
@@ -62,9 +64,9 @@ __global__ void __launch_bounds__(256) k_lift_dmma(const double* __restrict__ X,
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
       const int64_t p = p0 + t * 8 + 2 * (lane & 3);
-      if (NODE_MAJOR) {
-        if (p < P) x[i * ldx + p] = acc[t][0];
-        if (p + 1 < P) x[i * ldx + p + 1] = acc[t][1];
+      if (BLK16) {
+        if (p < P) x[((p >> 4) * n + i) * 16 + (p & 15)] = acc[t][0];
+        if (p + 1 < P) x[(((p + 1) >> 4) * n + i) * 16 + ((p + 1) & 15)] = acc[t][1];
       } else {
         if (p < P) x[p * n + i] = acc[t][0];
         if (p + 1 < P) x[(p + 1) * n + i] = acc[t][1];
@@ -72,12 +74,6 @@ __global__ void __launch_bounds__(256) k_lift_dmma(const double* __restrict__ X,
     }
   }
 }
-
-// Stencil residual on a materialised x (P x n): kResidPB parameter values per
-// blockIdx.y share each node's phi / neighbour reads; partial sums of
-// |Ax - b|^2 and |b|^2 per CTA and parameter (defined below).  The verification
-// residual only needs 3 significant digits (cli.py:344-351), so the edge
-// coefficients use the table exp and a reciprocal multiply.
 
 constexpr int kLiftPT = 8;  // parameter values per CTA
 
@@ -217,66 +213,109 @@ __global__ void k_resid_finish(const double* __restrict__ part, int nb, int64_t 
   relres[p] = sqrt(rr) / fmax(sqrt(bb), 1e-300);
 }
 
-constexpr int kResidPB = 16;  // parameter values per thread pass (amortises the phi / nbr reads)
+constexpr int kResidPB = 16;   // parameter values per pass: one 128-byte line of x per node
+constexpr int kResidTPN = 4;   // threads per node, kResidPB / kResidTPN parameter values each
+constexpr int kResidPT = kResidPB / kResidTPN;
 
-// grid = (nb, ceil(P / kResidPB)); x is node-major n x ldx (this chunk), params P x dp
-__global__ void __launch_bounds__(256) k_resid_stencil_x(const double* __restrict__ x, int64_t n, int64_t P,
-                                                         int64_t ldx,
-                                                         const int64_t* __restrict__ nbr,
-                                                         const double* __restrict__ phi, int E, int dp, double hh,
-                                                         const double* __restrict__ b,
-                                                         const double* __restrict__ params,
-                                                         double* __restrict__ part) {
+// Stencil residual for the 16 parameter values of pass blockIdx.y on the
+// blocked x (BLK16 layout of k_lift_dmma): per node i,
+//   r_i = sum_e c_e (x_i - x_{m_e}) - b_i   (x_m = 0 outside the domain, Dirichlet),
+//   c_e = exp(p . phi_{i,e}) / h^2,
+// i.e. (diag x_i + sum_e off_e x_m - b_i) of the reference's matrix_fn
+// (systems.py:306-334) regrouped: the verification residual needs 3
+// significant digits (cli.py:344-351), so the edge argument uses FMAs and the
+// table exp.  Eight consecutive lanes share a node (2 parameter values each):
+// x_i and x_m are whole aligned 128-byte lines read by 8 lanes, the node's phi
+// and neighbour indices are broadcast loads serving 16 parameter values.
+// grid = (nb, passes); partial sums of |r|^2 and |b|^2 per CTA and parameter.
+__global__ void __launch_bounds__(256, 2) k_resid_stencil_b16(const double* __restrict__ x, int64_t n, int64_t P,
+                                                           const int64_t* __restrict__ nbr,
+                                                           const double* __restrict__ phi, int E, int dp, double hh,
+                                                           const double* __restrict__ b,
+                                                           const double* __restrict__ params,
+                                                           double* __restrict__ part) {
   __shared__ double red[32];
   __shared__ double ps[kResidPB * 8];
   __shared__ double tab_s[2048];
+  __shared__ double rsum[kResidPB][8];
   for (int j = threadIdx.x; j < 2048; j += blockDim.x) tab_s[j] = g_exp2_tab2048[j];
   const double inv_hh = 1.0 / hh;
   const int64_t pb = (int64_t)blockIdx.y * kResidPB;
   const int npb = (int)((P - pb) < kResidPB ? (P - pb) : kResidPB);
-  for (int e = threadIdx.x; e < kResidPB * dp; e += blockDim.x) {
-    const int u = e / dp;
-    ps[e] = (u < npb) ? params[(pb + u) * dp + (e - u * dp)] : 0.0;
+  for (int e = threadIdx.x; e < kResidPB * 8; e += blockDim.x) {
+    const int u = e / 8, k = e - u * 8;
+    ps[e] = (u < npb && k < dp) ? params[(pb + u) * dp + k] : 0.0;
   }
   __syncthreads();
-  double rr[kResidPB];
+  const int sub = threadIdx.x % kResidTPN;  // which 4 parameter values of the line
+  const int u0 = sub * kResidPT;
+  const double2* xb = reinterpret_cast<const double2*>(x + (int64_t)blockIdx.y * n * kResidPB) + sub * (kResidPT / 2);
+  double pu[kResidPT][8];  // this thread's parameter values
 #pragma unroll
-  for (int u = 0; u < kResidPB; ++u) rr[u] = 0.0;
+  for (int u = 0; u < kResidPT; ++u)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) pu[u][k] = ps[(u0 + u) * 8 + k];
+  double rr[kResidPT];
+#pragma unroll
+  for (int u = 0; u < kResidPT; ++u) rr[u] = 0.0;
   double bb = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double diag[kResidPB], off[kResidPB];
+  const int64_t nstride = (int64_t)gridDim.x * blockDim.x / kResidTPN;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kResidTPN; i < n; i += nstride) {
+    double xi[kResidPT], acc[kResidPT];
 #pragma unroll
-    for (int u = 0; u < kResidPB; ++u) diag[u] = off[u] = 0.0;
+    for (int h = 0; h < kResidPT / 2; ++h) {
+      const double2 v = __ldg(xb + i * (kResidPB / 2) + h);
+      xi[2 * h] = v.x;
+      xi[2 * h + 1] = v.y;
+    }
+#pragma unroll
+    for (int u = 0; u < kResidPT; ++u) acc[u] = 0.0;
     for (int e = 0; e < E; ++e) {
       const double* ph = phi + (i * E + e) * dp;
       double phv[8];
-      for (int k = 0; k < dp; ++k) phv[k] = __ldg(ph + k);
-      const int64_t m = __ldg(nbr + i * E + e);
 #pragma unroll
-      for (int u = 0; u < kResidPB; ++u) {
-        if (u >= npb) break;
-        double arg = dmul_exact(ps[u * dp], phv[0]);
-        for (int k = 1; k < dp; ++k) arg = dadd_exact(arg, dmul_exact(ps[u * dp + k], phv[k]));
-        const double c = sas_exp64_t2k(arg, tab_s) * inv_hh;  // checker: a few ulp suffice
-        diag[u] += c;
-        if (m >= 0) off[u] = fma(-c, __ldg(x + m * ldx + pb + u), off[u]);
+      for (int k = 0; k < 8; ++k) phv[k] = (k < dp) ? __ldg(ph + k) : 0.0;
+      const int64_t m = __ldg(nbr + i * E + e);
+      double xm[kResidPT];
+#pragma unroll
+      for (int h = 0; h < kResidPT / 2; ++h) {
+        const double2 v = (m >= 0) ? __ldg(xb + m * (kResidPB / 2) + h) : make_double2(0.0, 0.0);
+        xm[2 * h] = v.x;
+        xm[2 * h + 1] = v.y;
+      }
+#pragma unroll
+      for (int u = 0; u < kResidPT; ++u) {
+        double arg = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k < dp) arg = fma(pu[u][k], phv[k], arg);
+        const double c = sas_exp64_t2k(arg, tab_s) * inv_hh;
+        acc[u] = fma(c, xi[u] - xm[u], acc[u]);
       }
     }
-    const double bi = b[i];
+    const double bi = __ldg(b + i);
 #pragma unroll
-    for (int u = 0; u < kResidPB; ++u) {
-      if (u >= npb) break;
-      const double res = fma(diag[u], x[i * ldx + pb + u], off[u]) - bi;
+    for (int u = 0; u < kResidPT; ++u) {
+      const double res = acc[u] - bi;
       rr[u] = fma(res, res, rr[u]);
     }
-    bb = fma(bi, bi, bb);
+    if (sub == 0) bb = fma(bi, bi, bb);
   }
-  const double tbb = block_sum(bb, red);
-  for (int u = 0; u < npb; ++u) {
-    const double trr = block_sum(rr[u], red);
-    if (threadIdx.x == 0) {
-      part[((pb + u) * gridDim.x + blockIdx.x) * 2] = trr;
-      part[((pb + u) * gridDim.x + blockIdx.x) * 2 + 1] = tbb;
-    }
+  // per parameter: sum over the lanes with the same sub (xor 8, 16), then warps
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int u = 0; u < kResidPT; ++u) {
+    double v = rr[u];
+#pragma unroll
+    for (int off = kResidTPN; off < 32; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (lane < kResidTPN) rsum[u0 + u][warp] = v;
   }
+  const double tbb = block_sum(bb, red);  // (its __syncthreads also publishes rsum)
+  if (threadIdx.x < npb) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += rsum[threadIdx.x][w];
+    part[((pb + threadIdx.x) * gridDim.x + blockIdx.x) * 2] = t;
+  }
+  if (threadIdx.x == 0)
+    for (int u = 0; u < npb; ++u) part[((pb + u) * gridDim.x + blockIdx.x) * 2 + 1] = tbb;
 }

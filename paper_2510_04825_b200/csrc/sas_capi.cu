@@ -982,18 +982,19 @@ extern "C" int sas_solve_host(sas_plan* pl, const void* params, int64_t P, const
 
 // x = X c for P parameters: P x n (node_major = false) or n x ldx (node_major = true)
 static int launch_lift_dmma(sas_plan* pl, const double* coef, int64_t P, double* x, cudaStream_t st,
-                            bool node_major = false, int64_t ldx = 0) {
+                            bool blk16 = false) {
   const size_t smem = 2 * (size_t)kLiftNodes * lift_ld(pl->r) * sizeof(double);
   SAS_CUDA_CHECK(cudaFuncSetAttribute(k_lift_dmma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   SAS_CUDA_CHECK(cudaFuncSetAttribute(k_lift_dmma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   for (int64_t p0 = 0; p0 < P; p0 += 65535LL * kLiftPar) {
     const int64_t pc = (P - p0 < 65535LL * kLiftPar) ? P - p0 : 65535LL * kLiftPar;
     dim3 grid((unsigned)((pl->n + kLiftNodes - 1) / kLiftNodes), (unsigned)((pc + kLiftPar - 1) / kLiftPar));
-    if (node_major)
-      k_lift_dmma<true><<<grid, 256, smem, st>>>((const double*)pl->X, pl->n, pl->r, coef + p0 * pl->r, pc, x + p0, ldx);
+    if (blk16)  // p0 is a multiple of 16: the blocks of this launch start at block p0 / 16
+      k_lift_dmma<true><<<grid, 256, smem, st>>>((const double*)pl->X, pl->n, pl->r, coef + p0 * pl->r, pc,
+                                                 x + p0 * pl->n);
     else
       k_lift_dmma<false><<<grid, 256, smem, st>>>((const double*)pl->X, pl->n, pl->r, coef + p0 * pl->r, pc,
-                                                  x + p0 * pl->n, 0);
+                                                  x + p0 * pl->n);
   }
   SAS_CUDA_CHECK(cudaGetLastError());
   return SAS_OK;
@@ -1092,19 +1093,18 @@ extern "C" int sas_residual(sas_plan* pl, const void* params, const void* coef, 
   pl->last_launches = 0;
   dim3 grid(nb, (unsigned)P);
   if (pl->op == SAS_OP_STENCIL) {
-    // x for a chunk of parameters (K5, DMMA), then the stencil residual on it (K6);
-    // the chunk keeps the x scratch within ~2 GB
+    // x for a chunk of (up to) 64 parameters (K5, DMMA, one X pass per chunk),
+    // stored in 16-parameter blocks, then the stencil residual on it (K6)
     ARG_CHECK(pl->full_nbr, "sas_residual: stencil operator not set");
-    int64_t chunk = (2ll << 30) / (pl->n * (int64_t)sizeof(double));
-    chunk = chunk < 1 ? 1 : (chunk > P ? P : chunk);
+    const int64_t chunk = P < 64 ? ((P + kResidPB - 1) / kResidPB) * kResidPB : 64;
     if ((rc = ensure(&pl->xscr, &pl->xscr_n, chunk * pl->n * (int64_t)sizeof(double)))) return rc;
     for (int64_t p0 = 0; p0 < P; p0 += chunk) {
       const int64_t pc = (P - p0 < chunk) ? P - p0 : chunk;
-      if ((rc = launch_lift_dmma(pl, (const double*)coef + p0 * pl->r, pc, pl->xscr, st, true, pc))) return rc;
+      if ((rc = launch_lift_dmma(pl, (const double*)coef + p0 * pl->r, pc, pl->xscr, st, true))) return rc;
       dim3 g2(nb, (unsigned)((pc + kResidPB - 1) / kResidPB));
-      k_resid_stencil_x<<<g2, 256, 0, st>>>(pl->xscr, pl->n, pc, pc, pl->full_nbr, pl->full_phi, pl->E, pl->dp, pl->hh,
-                                            (const double*)pl->full_b, (const double*)params + p0 * pl->dp,
-                                            pl->rpart + p0 * nb * 2);
+      k_resid_stencil_b16<<<g2, 256, 0, st>>>(pl->xscr, pl->n, pc, pl->full_nbr, pl->full_phi, pl->E, pl->dp, pl->hh,
+                                              (const double*)pl->full_b, (const double*)params + p0 * pl->dp,
+                                              pl->rpart + p0 * nb * 2);
       pl->last_launches += 2;
     }
   } else if (pl->op == SAS_OP_AFFINE) {
