@@ -43,7 +43,7 @@ __device__ __forceinline__ double f(double dv, double b, float bf, const double*
 template <int MODE, int PW, int NT>
 __global__ void __launch_bounds__(320, 2) k_mix(double* out, int iters, double d0) {
   __shared__ double tab_s[2048];
-  for (int j = threadIdx.x; j < 2048; j += blockDim.x) tab_s[j] = g_exp2_tab2048[j];
+  for (int j = threadIdx.x; j < 2048; j += blockDim.x) tab_s[j] = -g_exp2_tab2048[j];  // negated (sas_exp64_t2k_fr)
   __syncthreads();
   const int lane = threadIdx.x & 31;
   double b[PW]; float bf[PW];
