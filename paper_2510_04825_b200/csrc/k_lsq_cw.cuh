@@ -99,29 +99,49 @@ struct CwStep {
   static __device__ __forceinline__ void run(double (&A)[RA][NCW], int k, int kw, int warp, int lane, int r,
                                              const CwShared& sh) {
     constexpr int NA = NCW - C0;
-    constexpr int N2 = cw_pow2(NA);
-    constexpr int SH = 5 - cw_log2(N2);
+    // columns in groups of at most 8, one reduce-scatter each
+    constexpr int NA1 = NA < 8 ? NA : 8, NA2 = NA - NA1;
+    constexpr int N21 = cw_pow2(NA1), N22 = cw_pow2(NA2 > 0 ? NA2 : 1);
+    constexpr int SH1 = 5 - cw_log2(N21), SH2 = 5 - cw_log2(N22);
     const int buf = k & 1;
     const double* vb = sh.vbuf + buf * 32 * RA;
     const double tau = sh.scal[2 * buf];
     double v[RA];
 #pragma unroll
     for (int u = 0; u < RA; ++u) v[u] = vb[lane + 32 * u];
-    double d[N2];
+    double d1[N21];
 #pragma unroll
-    for (int c = 0; c < N2; ++c) {
+    for (int c = 0; c < N21; ++c) {
       double acc = 0.0;
-      if (c < NA) {
+      if (c < NA1) {
 #pragma unroll
         for (int u = 0; u < RA; ++u) acc = fma(v[u], A[u][C0 + c], acc);
       }
-      d[c] = acc;
+      d1[c] = acc;
     }
-    const double wl = tau * warp_reduce_scatter<N2>(d, lane);
+    const double wl1 = tau * warp_reduce_scatter<N21>(d1, lane);
+    double wl2 = 0.0;
+    if constexpr (NA2 > 0) {
+      double d2[N22];
+#pragma unroll
+      for (int c = 0; c < N22; ++c) {
+        double acc = 0.0;
+        if (c < NA2) {
+#pragma unroll
+          for (int u = 0; u < RA; ++u) acc = fma(v[u], A[u][C0 + NA1 + c], acc);
+        }
+        d2[c] = acc;
+      }
+      wl2 = tau * warp_reduce_scatter<N22>(d2, lane);
+    }
     const bool pivot_done = warp <= kw;  // slot C0 holds column warp + W*C0 <= k
 #pragma unroll
     for (int c = 0; c < NA; ++c) {
-      double w = __shfl_sync(0xffffffffu, wl, c << SH);
+      double w;
+      if (c < NA1)  // resolved at compile time (c is an unrolled index)
+        w = __shfl_sync(0xffffffffu, wl1, c << SH1);
+      else
+        w = __shfl_sync(0xffffffffu, wl2, (c - NA1) << SH2);
       if (c == 0 && pivot_done) w = 0.0;
 #pragma unroll
       for (int u = 0; u < RA; ++u) A[u][C0 + c] = fma(-v[u], w, A[u][C0 + c]);
@@ -152,27 +172,35 @@ struct CwColumns {
   }
 };
 
-__host__ __device__ inline size_t lsq_cw_smem_bytes(int s, int r, int RA, size_t scratch) {
+__host__ __device__ inline size_t lsq_cw_smem_bytes(int s, int r, int RA, size_t scratch, bool park = false) {
   const int ldm = r + 1;
-  // Ms (s x ldm), R/y (r x ldm), c, R_kk, 2 reflector vectors, 2 x {tau, beta}
-  size_t n = (size_t)s * ldm + (size_t)r * ldm + 2 * (size_t)r + 2 * 32 * (size_t)RA + 4;
+  // Ms (s x ldm), R/y (r x ldm; aliases Ms when parked), c, R_kk, 2 reflector
+  // vectors, 2 x {tau, beta}
+  size_t n = (size_t)s * ldm + (park ? 0 : (size_t)r * ldm) + 2 * (size_t)r + 2 * 32 * (size_t)RA + 4;
   size_t bytes = (n * sizeof(double) + 15) / 16 * 16;
   return bytes + kLsqRedDoubles * sizeof(double) + (scratch + 15) / 16 * 16;
 }
 
-template <int RA, int NCW, int W, class Asm>
-__global__ void __launch_bounds__(32 * W) k_lsq_cw(LsqArgs<double> a, Asm as, size_t scratch_bytes) {
+// PARK: the unweighted M (needed only by the explicit sampled residual at the
+// end) is copied to this CTA's global (L2) slot mglob after the load into
+// registers, and R reuses its shared-memory buffer: two CTAs per SM for the
+// 200 x 51 shape (lsq_cw_smem_bytes(..., park = true)).
+template <int RA, int NCW, int W, class Asm, int MINB = 1, bool PARK = false>
+__global__ void __launch_bounds__(32 * W, MINB) k_lsq_cw(LsqArgs<double> a, Asm as, size_t scratch_bytes,
+                                                         double* __restrict__ mglob = nullptr) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int s = a.s, r = a.r, ldm = r + 1;
   double* Ms = reinterpret_cast<double*>(smem_raw);
-  double* Rs = Ms + (size_t)s * ldm;
-  double* cvec = Rs + (size_t)r * ldm;
+  double* Rs = PARK ? Ms : Ms + (size_t)s * ldm;
+  double* cvec = Ms + (size_t)s * ldm + (PARK ? 0 : (size_t)r * ldm);
   CwShared sh;
   sh.rdiag = cvec + r;
   sh.vbuf = sh.rdiag + r;
   sh.scal = sh.vbuf + 2 * 32 * RA;
-  const size_t core = ((size_t)s * ldm + (size_t)r * ldm + 2 * (size_t)r + 2 * 32 * (size_t)RA + 4) * sizeof(double);
+  const size_t core =
+      ((size_t)s * ldm + (PARK ? 0 : (size_t)r * ldm) + 2 * (size_t)r + 2 * 32 * (size_t)RA + 4) * sizeof(double);
+  double* mg = PARK ? mglob + (size_t)blockIdx.x * s * ldm : Ms;
   double* red = reinterpret_cast<double*>(smem_raw + (core + 15) / 16 * 16);  // residual partials (<= 16)
   sh.nrm_s = red + 16;
   double* rinfo = sh.nrm_s + 64;
@@ -203,6 +231,8 @@ __global__ void __launch_bounds__(32 * W) k_lsq_cw(LsqArgs<double> a, Asm as, si
         A[u][c] = m;
       }
     }
+    if (PARK)
+      for (int idx = threadIdx.x; idx < s * ldm; idx += blockDim.x) mg[idx] = Ms[idx];
     if (__syncthreads_or(bad)) {
       lsq_nonfinite<double>(a, p);
       continue;
@@ -221,6 +251,6 @@ __global__ void __launch_bounds__(32 * W) k_lsq_cw(LsqArgs<double> a, Asm as, si
         if (i < r && j > i && j <= r) Rs[i * ldm + j] = A[u][c];
       }
     }
-    lsq_finish<double>(a, p, Ms, ldm, Rs, cvec, sh.rdiag, sh.nrm_s, rinfo, red, W);
+    lsq_finish<double>(a, p, mg, ldm, Rs, cvec, sh.rdiag, sh.nrm_s, rinfo, red, W);
   }
 }

@@ -184,6 +184,8 @@ struct sas_plan {
   void** csr_va_d = nullptr;
   // scratch
   double* Mscr = nullptr;
+  double* cw_mg = nullptr;   // K4 column-owner kernel (PARK): per-CTA slots for the unweighted M
+  int64_t cw_mg_n = 0;
   int64_t Mscr_P = 0;
   double* rpart = nullptr;
   int64_t rpart_n = 0;
@@ -284,7 +286,7 @@ static void plan_free(sas_plan* pl) {
   DevGuard g(pl->device);
   void* ptrs[] = {pl->X, pl->S, pl->w, pl->t, pl->proj, pl->kind, pl->scale, pl->rate, pl->blocks,
                   pl->phi, pl->G, pl->gmap, pl->pts, pl->D, pl->Dfrag, pl->Xfrag, pl->full_nbr, pl->full_phi, pl->full_b,
-                  pl->csr_rp_d, pl->csr_ci_d, pl->csr_va_d, pl->Mscr, pl->rpart, pl->xscr, pl->fco,
+                  pl->csr_rp_d, pl->csr_ci_d, pl->csr_va_d, pl->Mscr, pl->cw_mg, pl->rpart, pl->xscr, pl->fco,
                   pl->h_params, pl->h_ctab, pl->h_rhs, pl->h_coef, pl->h_sres, pl->h_outv,
                   pl->h_status, pl->h_bad};
   for (void* p : ptrs)
@@ -645,10 +647,10 @@ static int launch_lsq_mw_t(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, siz
   return SAS_OK;
 }
 
-template <int RA, int NCW, int W, class Asm>
+template <int RA, int NCW, int W, int MINB = 1, bool PARK = false, class Asm>
 static int launch_lsq_cw_t(sas_plan* pl, const LsqArgs<double>& a, const Asm& as, size_t scratch, cudaStream_t st) {
-  const size_t smem = lsq_cw_smem_bytes(a.s, a.r, RA, scratch);
-  auto kern = k_lsq_cw<RA, NCW, W, Asm>;
+  const size_t smem = lsq_cw_smem_bytes(a.s, a.r, RA, scratch, PARK);
+  auto kern = k_lsq_cw<RA, NCW, W, Asm, MINB, PARK>;
   SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
   int occ = 0;
@@ -660,8 +662,14 @@ static int launch_lsq_cw_t(sas_plan* pl, const LsqArgs<double>& a, const Asm& as
   int64_t grid = (int64_t)occ * pl->sms;
   if (grid > a.P) grid = a.P;
   if (grid < 1) grid = 1;
+  double* mg = nullptr;
+  if (PARK) {
+    const int rc = ensure(&pl->cw_mg, &pl->cw_mg_n, grid * a.s * (int64_t)(a.r + 1) * (int64_t)sizeof(double));
+    if (rc) return rc;
+    mg = pl->cw_mg;
+  }
   stage_begin(pl, st, SAS_STAGE_LSQ);
-  kern<<<(unsigned)grid, 32 * W, smem, st>>>(a, as, scratch);
+  kern<<<(unsigned)grid, 32 * W, smem, st>>>(a, as, scratch, mg);
   stage_end(pl, st);
   SAS_CUDA_CHECK(cudaGetLastError());
   pl->last_launches++;
@@ -670,10 +678,11 @@ static int launch_lsq_cw_t(sas_plan* pl, const LsqArgs<double>& a, const Asm& as
 
 // Column-owner variants (rows <= 32*RA, columns <= NCW*W) for real shapes
 // with r+1 > 32, in preference order (config 3: {5,7,6} 5.94 ms vs 6.84 ms
-// for k_lsq_mw; config 5: {7,5,12} 14.5 ms vs 17.6 ms, 32,768 p);
+// for k_lsq_mw, 32,768 p; config 5: {7,9,6} with M parked in L2 runs two
+// CTAs per SM, 40 ms vs 55 ms for {7,5,12} at 125,000 p);
 // SAS_LSQ_CW=<index> forces one (tuning), SAS_LSQ_CW=off disables them.
 struct CwVariant { int ra, ncw, w; };
-static const CwVariant kCwVariants[] = {{5, 7, 6}, {5, 6, 8}, {7, 5, 12}, {7, 4, 16}};
+static const CwVariant kCwVariants[] = {{5, 7, 6}, {5, 6, 8}, {7, 9, 6}, {7, 5, 12}, {7, 4, 16}};
 static int lsq_cw_env() {
   static int v = -3;
   if (v == -3) {
@@ -686,9 +695,10 @@ template <class Asm>
 static int launch_lsq_cw_idx(sas_plan* pl, const LsqArgs<double>& a, const Asm& as, size_t scratch, cudaStream_t st,
                              int idx) {
   switch (idx) {
-    case 0: return launch_lsq_cw_t<5, 7, 6>(pl, a, as, scratch, st);
+    case 0: return launch_lsq_cw_t<5, 7, 6, 2>(pl, a, as, scratch, st);  // 2 CTAs/SM (<= 170 registers)
     case 1: return launch_lsq_cw_t<5, 6, 8>(pl, a, as, scratch, st);
-    case 2: return launch_lsq_cw_t<7, 5, 12>(pl, a, as, scratch, st);
+    case 2: return launch_lsq_cw_t<7, 9, 6, 2, true>(pl, a, as, scratch, st);  // 2 CTAs/SM: M parked in L2
+    case 3: return launch_lsq_cw_t<7, 5, 12>(pl, a, as, scratch, st);
     default: return launch_lsq_cw_t<7, 4, 16>(pl, a, as, scratch, st);
   }
 }
