@@ -192,9 +192,9 @@ struct AsmStencil {
   const int8_t* gmap;   // s x (E+1)
   double hh;
   const double* params;  // P x dp (real)
-  // per row: edge coefficients (8 doubles), then the coefficient of each
-  // gathered row in G order (8 doubles, zero for padding slots)
-  static size_t scratch_bytes(int s, int) { return (size_t)s * 16 * sizeof(double); }
+  // per row 8 doubles: the diagonal and edge coefficients, then (rewritten in
+  // place) the coefficient of each gathered row in G order (zero for padding)
+  static size_t scratch_bytes(int s, int) { return (size_t)s * 8 * sizeof(double); }
   template <class Grp>
   __device__ __forceinline__ void operator()(const Grp& g, int64_t p, double* Ms, int ldm, int s, int r,
                                              unsigned char* scratch) const {
@@ -204,7 +204,7 @@ struct AsmStencil {
     // one row per thread: edge coefficients, the diagonal (edge order), then
     // the signed coefficient of every gathered row
     for (int i = g.rank(); i < s; i += g.size()) {
-      double* ci = cs + i * 16;
+      double* ci = cs + i * 8;
       double d = 0.0;
       for (int e = 0; e < E; ++e) {
         const double* ph = phi + ((int64_t)i * E + e) * dp;
@@ -216,11 +216,14 @@ struct AsmStencil {
       }
       ci[0] = d;
       const int8_t* mp = gmap + i * E1;
+      double nv[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int slot = (q < E1) ? mp[q] : -1;
-        ci[8 + q] = (slot < 0) ? 0.0 : (slot == 0 ? d : -ci[slot]);
+        nv[q] = (slot < 0) ? 0.0 : (slot == 0 ? d : -ci[slot]);
       }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) ci[q] = nv[q];
     }
     g.sync();
     // M = rows @ G in ascending column order with FMA (padding slots add
@@ -245,7 +248,7 @@ struct AsmStencil {
 #pragma unroll
       for (int t = 0; t < kUnroll; ++t) {
         if (base + t * g.size() < total) {
-          const double2* a2 = reinterpret_cast<const double2*>(cs + ii[t] * 16 + 8);
+          const double2* a2 = reinterpret_cast<const double2*>(cs + ii[t] * 8);
           double m = 0.0;
 #pragma unroll
           for (int q2 = 0; q2 < 4; ++q2) {

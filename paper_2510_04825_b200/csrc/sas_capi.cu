@@ -682,7 +682,7 @@ static int launch_lsq_cw_t(sas_plan* pl, const LsqArgs<double>& a, const Asm& as
 // CTAs per SM, 40 ms vs 55 ms for {7,5,12} at 125,000 p);
 // SAS_LSQ_CW=<index> forces one (tuning), SAS_LSQ_CW=off disables them.
 struct CwVariant { int ra, ncw, w; };
-static const CwVariant kCwVariants[] = {{5, 7, 6}, {5, 6, 8}, {7, 9, 6}, {7, 5, 12}, {7, 4, 16}};
+static const CwVariant kCwVariants[] = {{5, 11, 4}, {5, 7, 6}, {5, 6, 8}, {7, 9, 6}, {7, 5, 12}, {7, 4, 16}};
 static int lsq_cw_env() {
   static int v = -3;
   if (v == -3) {
@@ -695,10 +695,11 @@ template <class Asm>
 static int launch_lsq_cw_idx(sas_plan* pl, const LsqArgs<double>& a, const Asm& as, size_t scratch, cudaStream_t st,
                              int idx) {
   switch (idx) {
-    case 0: return launch_lsq_cw_t<5, 7, 6, 2>(pl, a, as, scratch, st);  // 2 CTAs/SM (<= 170 registers)
-    case 1: return launch_lsq_cw_t<5, 6, 8>(pl, a, as, scratch, st);
-    case 2: return launch_lsq_cw_t<7, 9, 6, 2, true>(pl, a, as, scratch, st);  // 2 CTAs/SM: M parked in L2
-    case 3: return launch_lsq_cw_t<7, 5, 12>(pl, a, as, scratch, st);
+    case 0: return launch_lsq_cw_t<5, 11, 4, 3, true>(pl, a, as, scratch, st);  // 3 CTAs/SM: M parked in L2
+    case 1: return launch_lsq_cw_t<5, 7, 6, 2>(pl, a, as, scratch, st);  // 2 CTAs/SM (<= 170 registers)
+    case 2: return launch_lsq_cw_t<5, 6, 8>(pl, a, as, scratch, st);
+    case 3: return launch_lsq_cw_t<7, 9, 6, 2, true>(pl, a, as, scratch, st);  // 2 CTAs/SM: M parked in L2
+    case 4: return launch_lsq_cw_t<7, 5, 12>(pl, a, as, scratch, st);
     default: return launch_lsq_cw_t<7, 4, 16>(pl, a, as, scratch, st);
   }
 }
