@@ -99,6 +99,25 @@ struct AsmGlobal {
                                              unsigned char*) const {
     const T* src = M + p * (int64_t)s * r;
     RowMajorWalk wk(g.rank(), g.size(), r);
+    if (nsplit == 2) {  // K3's split-K partials: loads of 4 entries issued before their adds
+      constexpr int U = 4;
+      const int total = s * r, step = g.size();
+      for (int base = g.rank(); base < total; base += U * step) {
+        T v0[U], v1[U];
+#pragma unroll
+        for (int t = 0; t < U; ++t) {
+          const int idx = base + t * step;
+          v0[t] = idx < total ? src[idx] : T{};
+          v1[t] = idx < total ? src[idx + split] : T{};
+        }
+#pragma unroll
+        for (int t = 0; t < U; ++t) {
+          if (base + t * step < total) Ms[wk.i * ldm + wk.j] = v0[t] + v1[t];
+          wk.next();
+        }
+      }
+      return;
+    }
     for (int idx = g.rank(); idx < s * r; idx += g.size(), wk.next()) {
       T v = src[idx];
       for (int z = 1; z < nsplit; ++z) v = v + src[idx + z * split];
