@@ -220,19 +220,24 @@ struct AsmStencil {
     double* cs = reinterpret_cast<double*>(scratch);
     const double* pp = params + p * dp;
     const int E1 = E + 1;
-    // one row per thread: edge coefficients, the diagonal (edge order), then
-    // the signed coefficient of every gathered row
+    // edge coefficients, one (row, edge) per thread and pass: the exp/division
+    // chains are independent, so a thread's two unrolled passes overlap
+    const int se = s * E;
+#pragma unroll 2
+    for (int idx = g.rank(); idx < se; idx += g.size()) {
+      const int i = idx / E, e = idx - i * E;
+      const double* ph = phi + (int64_t)idx * dp;
+      double arg = dmul_exact(pp[0], ph[0]);
+      for (int k = 1; k < dp; ++k) arg = dadd_exact(arg, dmul_exact(pp[k], ph[k]));
+      cs[i * 8 + 1 + e] = exp(arg) / hh;
+    }
+    g.sync();
+    // per row: the diagonal (edge order), then the signed coefficient of every
+    // gathered row
     for (int i = g.rank(); i < s; i += g.size()) {
       double* ci = cs + i * 8;
       double d = 0.0;
-      for (int e = 0; e < E; ++e) {
-        const double* ph = phi + ((int64_t)i * E + e) * dp;
-        double arg = dmul_exact(pp[0], ph[0]);
-        for (int k = 1; k < dp; ++k) arg = dadd_exact(arg, dmul_exact(pp[k], ph[k]));
-        const double c = exp(arg) / hh;
-        ci[1 + e] = c;
-        d = dadd_exact(d, c);
-      }
+      for (int e = 0; e < E; ++e) d = dadd_exact(d, ci[1 + e]);
       ci[0] = d;
       const int8_t* mp = gmap + i * E1;
       double nv[8];

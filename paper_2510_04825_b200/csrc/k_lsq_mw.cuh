@@ -306,8 +306,19 @@ __device__ __forceinline__ void lsq_finish(const LsqArgs<T>& a, int64_t p, const
   // sampled residual ||w (M c - t)|| from the unweighted M (online.py:121-124)
   double ss = 0.0;
   for (int i = threadIdx.x; i < s; i += blockDim.x) {
-    T acc = S::zero();
-    for (int j = 0; j < r; ++j) acc = S::add(acc, S::mul(Ms[i * ldm + j], cvec[j]));
+    // four interleaved partial sums (j mod 4), combined in a fixed order: the
+    // row loads (from L2 when M is parked) overlap instead of one chain
+    T a4[4] = {S::zero(), S::zero(), S::zero(), S::zero()};
+    const T* mrow = Ms + i * ldm;
+    int j = 0;
+    for (; j + 4 <= r; j += 4) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) a4[t] = S::add(a4[t], S::mul(mrow[j + t], cvec[j + t]));
+    }
+#pragma unroll
+    for (int t = 0; t < 3; ++t)
+      if (j + t < r) a4[t] = S::add(a4[t], S::mul(mrow[j + t], cvec[j + t]));
+    const T acc = S::add(S::add(a4[0], a4[1]), S::add(a4[2], a4[3]));
     T res = S::sub(acc, Ms[i * ldm + r]);
     if (a.w) res = S::mulr(res, a.w[i]);
     ss += S::abs2(res);
