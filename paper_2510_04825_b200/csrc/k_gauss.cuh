@@ -20,9 +20,10 @@
 // (mma.sync.m8n8k4.f64, SASS DMMA.8x8x4 — the only FP64 tensor shape on sm_100a;
 // FP64 has no tcgen05 kind).  D and X fragments stream through a 3-stage
 // shared-memory ring filled by bulk async copies (below) and are reused by all
-// PW parameters of the CTA.  The exp is sas_exp64_t2k_fr (5 FP64-pipe ops, the
-// range reduction on the FP32/integer pipes; DMMA and DFMA share one FP64 pipe
-// on B200, profiles/r01_fp64_peaks.jsonl).  Split-K over n (grid.z) removes the
+// PW parameters of the CTA.  The exp is sas_exp64_t2k_fast (5 FP64-pipe ops and
+// ~10 integer/FP32 instructions; CTAs whose arguments could underflow use the
+// masked sas_exp64_t2k_fr); DMMA and DFMA share one FP64 pipe on B200
+// (profiles/r01_fp64_peaks.jsonl).  Split-K over n (grid.z) removes the
 // partial last wave (1024 CTAs on 296 slots -> 2048 on 296).
 #pragma once
 #include "sas_common.cuh"
