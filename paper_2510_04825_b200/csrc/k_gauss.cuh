@@ -180,11 +180,29 @@ __host__ __device__ constexpr size_t gauss3_smem_bytes(int rows_cta) {
 // entry (the reference's exp(-0) + lam, _kernels.py:49).
 // Split-K: grid.z splits the n chunks into gridDim.z contiguous ranges whose
 // partial products go to Mout + z * msplit; K4 sums them in z order.
-template <int NT, int PW, int MINB, int MAXW>
+template <int NT, int PW, int MINB, int MAXW, int MODE = 0>
 __global__ void __launch_bounds__(32 * MAXW, MINB)
 k_gauss_rows(const double* __restrict__ Df, const double* __restrict__ Xf, const int64_t* __restrict__ S,
              const double* __restrict__ params, int dp, int64_t P, int s, int64_t nchunks, int r, double ridge,
              double* __restrict__ Mout, int64_t msplit, double dmax, const double* __restrict__ X) {
+  // parameter value = bandwidth sigma (dp == 1, plan ridge) or (lambda, sigma)
+  // (dp == 2, the reference's KRR system, systems.py:423-463)
+  const int64_t pbase = (int64_t)blockIdx.x * PW;
+  double ninv[PW];
+  float ninvf[PW];
+  double bmax = 0.0;
+#pragma unroll
+  for (int u = 0; u < PW; ++u) {
+    const int64_t p = pbase + u;
+    const double sg = (p < P) ? params[p * dp + dp - 1] : 1.0;
+    ninv[u] = -(1.0 / (2.0 * sg * sg));  // reference: inv = 1.0 / (2.0 * sigma * sigma)
+    ninvf[u] = (float)ninv[u];
+    bmax = fmax(bmax, -ninv[u]);
+  }
+  // MODE 0: both paths; 1: fast CTAs only (others return); 2: masked CTAs only.
+  // Decided before any bulk copy is issued.
+  const bool fast = dmax * bmax < SAS_EXP2K_FAST_MAX;
+  if ((MODE == 1 && !fast) || (MODE == 2 && fast)) return;
   extern __shared__ __align__(128) double gsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nrg = blockDim.x >> 5;            // row groups = warps
@@ -223,20 +241,6 @@ k_gauss_rows(const double* __restrict__ Df, const double* __restrict__ Xf, const
   if (threadIdx.x == 0)
     for (int64_t j = 0; j < kG3Stages - 1 && j < nloc; ++j) issue(j);
 
-  // parameter value = bandwidth sigma (dp == 1, plan ridge) or (lambda, sigma)
-  // (dp == 2, the reference's KRR system, systems.py:423-463)
-  const int64_t pbase = (int64_t)blockIdx.x * PW;
-  double ninv[PW];
-  float ninvf[PW];
-  double bmax = 0.0;
-#pragma unroll
-  for (int u = 0; u < PW; ++u) {
-    const int64_t p = pbase + u;
-    const double sg = (p < P) ? params[p * dp + dp - 1] : 1.0;
-    ninv[u] = -(1.0 / (2.0 * sg * sg));  // reference: inv = 1.0 / (2.0 * sigma * sigma)
-    ninvf[u] = (float)ninv[u];
-    bmax = fmax(bmax, -ninv[u]);
-  }
   auto lam_of = [&](int u) {
     const int64_t p = pbase + u;
     return (dp == 2) ? ((p < P) ? params[p * 2] : 0.0) : ridge;
@@ -245,7 +249,6 @@ k_gauss_rows(const double* __restrict__ Df, const double* __restrict__ Xf, const
   __syncthreads();
   const int grow = row0 + warp * 8 + (lane >> 2);
   const int64_t srow = (grow < s) ? S[grow] : -1;
-  const bool fast = dmax * bmax < SAS_EXP2K_FAST_MAX;
 
   double acc[PW][NT][2];
 #pragma unroll
@@ -253,7 +256,7 @@ k_gauss_rows(const double* __restrict__ Df, const double* __restrict__ Xf, const
 #pragma unroll
     for (int t = 0; t < NT; ++t) acc[u][t][0] = acc[u][t][1] = 0.0;
 
-  if (fast) {
+  if (MODE == 1 || (MODE == 0 && fast)) {
     for (int64_t j = 0; j < nloc; ++j) {
       if (threadIdx.x == 0 && j + kG3Stages - 1 < nloc) issue(j + kG3Stages - 1);
       const int b = (int)(j % kG3Stages);

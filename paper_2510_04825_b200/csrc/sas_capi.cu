@@ -788,6 +788,19 @@ static int gauss_ksplit(int64_t ctas, int64_t slots, int64_t nchunks) {
   return best;
 }
 
+// The fast and the masked CTAs run in two launches over the same grid (each
+// kernel carries one exponential path; a CTA of the other kind returns before
+// issuing any copy): 13.84 vs 13.90 ms on config 2.  SAS_K3_TWO=0: one kernel
+// with both paths.
+static bool k3_two_kernels() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SAS_K3_TWO");
+    v = (e && !atoi(e)) ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <int NT, int PW, int MINB, int MAXW = kGaussMaxWarps>
 static int launch_gauss_k(sas_plan* pl, const double* params, int64_t P, double* Mout, cudaStream_t st,
                           int* ksplit) {
@@ -799,20 +812,27 @@ static int launch_gauss_k(sas_plan* pl, const double* params, int64_t P, double*
     return SAS_ERR_ARG;
   }
   const size_t smem = gauss3_smem_bytes<NT>(rows_cta);
-  auto kern = k_gauss_rows<NT, PW, MINB, MAXW>;
-  SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  auto kern0 = k_gauss_rows<NT, PW, MINB, MAXW, 0>;
+  auto kern1 = k_gauss_rows<NT, PW, MINB, MAXW, 1>;
+  auto kern2 = k_gauss_rows<NT, PW, MINB, MAXW, 2>;
+  const bool two = k3_two_kernels();
+  for (auto kf : {kern0, kern1, kern2})
+    SAS_CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
-  SAS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * nw, smem));
+  SAS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, two ? kern1 : kern0, 32 * nw, smem));
   const int64_t nch = pl->n_pad / kGaussKC, ctas = ((P + PW - 1) / PW) * gy;
   const int z = gauss_ksplit(ctas, (int64_t)std::max(occ, 1) * pl->sms, nch);
   *ksplit = z;
   dim3 grid((unsigned)((P + PW - 1) / PW), (unsigned)gy, (unsigned)z);
   stage_begin(pl, st, SAS_STAGE_GAUSS_ROWS);
-  kern<<<grid, 32 * nw, smem, st>>>(pl->Dfrag, pl->Xfrag, pl->S, params, pl->dp, P, pl->s, nch, pl->r, pl->ridge,
+  for (int m = two ? 1 : 0; m <= (two ? 2 : 0); ++m) {
+    auto kf = m == 0 ? kern0 : (m == 1 ? kern1 : kern2);
+    kf<<<grid, 32 * nw, smem, st>>>(pl->Dfrag, pl->Xfrag, pl->S, params, pl->dp, P, pl->s, nch, pl->r, pl->ridge,
                                     Mout, P * pl->s * (int64_t)pl->r, pl->k3_dmax, (const double*)pl->X);
+    pl->last_launches++;
+  }
   stage_end(pl, st);
   SAS_CUDA_CHECK(cudaGetLastError());
-  pl->last_launches++;
   return SAS_OK;
 }
 
