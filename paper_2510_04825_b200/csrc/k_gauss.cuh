@@ -88,7 +88,7 @@ __host__ __device__ inline void gauss_row_blocks(int s, int maxw, int* gy, int* 
 // and fragment reads are conflict-free (lane-contiguous 8-byte loads).
 // ===========================================================================
 #ifndef K3_UNROLL
-#define K3_UNROLL 2
+#define K3_UNROLL 4
 #endif
 constexpr int kK3Unroll = K3_UNROLL;  // k-steps unrolled per loop iteration
 constexpr int kG3Stages = K3_STAGES;
