@@ -339,7 +339,8 @@ def main():
     step_dev_ms = local_ms / K
     roofline = {
         "bound": "tensor", "pipe": "FP64 DMMA.8x8x4 (shared with DFMA)",
-        "kernel": "k_gauss_rows (K3)", "achieved": round(achieved, 3), "peak": FP64_DMMA_PEAK_TFLOPS,
+        "kernel": "k_gauss_rows (K3; timed over its fast-exp and masked-exp launches, CUDA events on the "
+                  "launching stream)", "achieved": round(achieved, 3), "peak": FP64_DMMA_PEAK_TFLOPS,
         "peak_source": "measured FP64 DMMA microbenchmark on this pool (profiles/r01_fp64_peaks.jsonl); "
                        "MEASURED_PEAKS.json has no FP64 entry",
         "unit": "TFLOP/s", "frac": round(achieved / FP64_DMMA_PEAK_TFLOPS, 4),
