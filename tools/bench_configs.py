@@ -4,10 +4,9 @@
 
 For each config: build the problem at its BASELINE size, obtain X and S
 (offline: host sparse solves for config 1, GPU Cholesky for config 2, GPU CG
-for configs 3 and 5; config 4 (complex, non-symmetric) uses a seeded
-orthonormal synthetic basis because its snapshot solves are impractical here --
-the online cost does not depend on the values of X; --synthetic uses one for
-every config but 2), then time the device-resident online sweep of the
+for configs 3 and 5, GPU BiCGSTAB for config 4; --synthetic uses a seeded
+orthonormal basis for every config but 2 -- the online cost does not depend
+on the values of X), then time the device-resident online sweep of the
 config's per-GPU parameter count and compare a few parameters against the CPU
 oracle at full size.  One JSON line per config.
 """
@@ -90,8 +89,8 @@ def run(cfg, steps, dev, synthetic=False, P=None, check=True, resid_count=0):
         basis, sel = offline(prob, device=dev, prefer_cg=True)
         src = "offline (GPU CG snapshots)"
     elif cfg == 4:
-        basis, sel = synthetic_basis(prob, 8, complex_=True, device=dev)
-        src = "synthetic orthonormal basis r'=8 (complex)"
+        basis, sel = offline(prob, device=dev)
+        src = "offline (GPU BiCGSTAB snapshots, pod(1e-13))"
 
     t_off = time.perf_counter() - t0
     plan = online.precompute_online(prob.system, basis, sel, device=0)
