@@ -131,3 +131,30 @@ def test_gauss_rows_fast_and_underflow_paths():
         floor = online_ref.ls_floor(m, t, sel.weights)
         d = np.linalg.norm(res.coefficients[k] - c) / np.linalg.norm(c)
         assert d <= max(1e-10, 10 * floor), (k, p, d, floor)
+
+
+@pytest.mark.parametrize("r", [3, 8, 13, 20, 29, 40, 57])
+def test_gauss_rows_every_column_tiling(r):
+    # K3 for every DMMA column-tile count (NT = 1..8) and partial last tiles,
+    # on a synthetic orthonormal basis, against the oracle
+    from paper_2510_04825_b200.offline import RowSelector, SnapshotBasis
+    prob = problems.gauss_krr(n=900, seed=5)
+    rng = np.random.default_rng(r)
+    q, _ = np.linalg.qr(rng.standard_normal((900, r)))
+    basis = SnapshotBasis(points=(), raw=q, basis=q, singular_values=np.ones(r))
+    s = max(2 * r, 24)
+    sel = RowSelector(indices=np.sort(rng.choice(900, size=s, replace=False)), n=900,
+                      weights=rng.uniform(0.5, 2.0, s))
+    plan = online.precompute_online(prob.system, basis, sel)
+    params = prob.test_params(9)
+    res = online.solve_params(plan, params)
+    assert np.all(res.status == 0)
+    op = prob.system.operator
+    fn = lambda qv, rows: online_ref.gauss_rows(op.points, rows, float(qv), op.ridge)
+    for k, p in enumerate(params):
+        m = online_ref.sampled_rows(fn, q, sel.indices, p)
+        t = prob.system.rhs(p, sel.indices)
+        c, _, _ = online_ref.solve_one(m, t, sel.weights)
+        floor = online_ref.ls_floor(m, t, sel.weights)
+        d = np.linalg.norm(res.coefficients[k] - c) / np.linalg.norm(c)
+        assert d <= max(1e-10, 10 * floor), (r, k, d, floor)
