@@ -75,6 +75,27 @@ def oracle_coef(prob, basis, sel, p):
     return c, sres, floor
 
 
+DMMA_PEAK_TF, DFMA_PEAK_TF = 37.0, 34.1  # measured on this pool (profiles/r01_fp64_peaks.jsonl)
+
+
+def algorithmic_flops(prob, r, s, complex_):
+    """Per parameter value: assembly of S A(p) X, and the
+    least squares (Householder QR 2sr^2 - 2/3 r^3, Q^T t 4sr - 2r^2, back
+    solve r^2, explicit residual 2sr); complex counts x4."""
+    sysm = prob.system
+    op = getattr(sysm, "operator", None)
+    ls = 2 * s * r * r - 2 * r ** 3 / 3 + 4 * s * r - 2 * r * r + r * r + 2 * s * r
+    if sysm.affine_terms is not None:
+        asm = 2 * len(sysm.affine_terms) * s * r
+    elif isinstance(op, GaussianKernelOperator):
+        asm = 2 * s * sysm.n * r
+    else:
+        E, dp = op.n_edges, op.n_params
+        asm = 2 * E * s * dp + 2 * (E + 1) * s * r
+    mul = 4 if complex_ else 1
+    return mul * asm, mul * ls
+
+
 def run(cfg, steps, dev, synthetic=False, P=None, check=True, resid_count=0):
     t0 = time.perf_counter()
     prob = problems.build(cfg)
@@ -147,8 +168,19 @@ def run(cfg, steps, dev, synthetic=False, P=None, check=True, resid_count=0):
             ref = online_ref.relative_residual(a, x, b)
             resid["relres0_gpu"] = float(rr[0])
             resid["relres0_oracle"] = ref
+    f_asm, f_ls = algorithmic_flops(prob, basis.rank, sel.size, g.complex)
+    st_ms = {("K3" if k == _capi.SAS_STAGE_GAUSS_ROWS else "K4"): sum(v) / steps for k, v in stage.items()}
+    roof = {"gflop_per_sweep": round((f_asm + f_ls) * P / 1e9, 3), "tflops_sweep": round((f_asm + f_ls) * P / ms / 1e9, 3)}
+    if "K3" in st_ms:  # contraction on DMMA, least squares (K4) on DFMA
+        roof["K3_tflops"] = round(f_asm * P / st_ms["K3"] / 1e9, 3)
+        roof["K3_frac_dmma_peak"] = round(roof["K3_tflops"] / DMMA_PEAK_TF, 4)
+        roof["K4_tflops"] = round(f_ls * P / st_ms["K4"] / 1e9, 3)
+        roof["K4_frac_dfma_peak"] = round(roof["K4_tflops"] / DFMA_PEAK_TF, 4)
+    else:  # assembly fused into K4
+        roof["K4_tflops"] = round((f_asm + f_ls) * P / st_ms["K4"] / 1e9, 3)
+        roof["K4_frac_dfma_peak"] = round(roof["K4_tflops"] / DFMA_PEAK_TF, 4)
     return {
-        "resid": resid,
+        "resid": resid, "roofline": roof,
         "config": cfg, "name": prob.key, "n": prob.system.n, "r": basis.rank, "s": sel.size, "P": P,
         "dtype": "c128" if g.complex else "f64", "basis": src, "offline_s": round(t_off, 1),
         "ms_per_sweep": round(ms, 3), "p_per_s": round(P / ms * 1e3, 1),
