@@ -77,7 +77,7 @@ __device__ __forceinline__ void cw_reflector(const double (&A)[RA][NCW], int k, 
   const double aa = fabs(alpha);
   double beta = 0.0, tau = 0.0;
   if (nrm != 0.0) {
-    beta = (aa == 0.0) ? -nrm : alpha * (-nrm * rcp_nr(aa));
+    beta = (aa == 0.0) ? -nrm : copysign(nrm, -alpha);  // -sign(x_k) |x| exactly (no reciprocal)
     tau = rcp_nr(nrm * (nrm + aa));
   }
   double* vb = sh.vbuf + buf * 32 * RA;
