@@ -28,7 +28,8 @@ def nvcc_path() -> str:
 
 
 def sources() -> list:
-    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + [HERE.parent / "include" / "sas.h"]
+    return (sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.inc"))
+            + [HERE.parent / "include" / "sas.h"])
 
 
 def up_to_date() -> bool:

@@ -26,24 +26,6 @@ static const double h_exp2_tab2048[2048] = {
 #include "exp2_table2048.inc"
 };
 
-static const double h_exp2_tab64[64] = {
-    0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
-    0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0,
-    0x1.172b83c7d517bp+0, 0x1.1a35beb6fcb75p+0, 0x1.1d4873168b9aap+0, 0x1.2063b88628cd6p+0,
-    0x1.2387a6e756238p+0, 0x1.26b4565e27cddp+0, 0x1.29e9df51fdee1p+0, 0x1.2d285a6e4030bp+0,
-    0x1.306fe0a31b715p+0, 0x1.33c08b26416ffp+0, 0x1.371a7373aa9cbp+0, 0x1.3a7db34e59ff7p+0,
-    0x1.3dea64c123422p+0, 0x1.4160a21f72e2ap+0, 0x1.44e086061892dp+0, 0x1.486a2b5c13cd0p+0,
-    0x1.4bfdad5362a27p+0, 0x1.4f9b2769d2ca7p+0, 0x1.5342b569d4f82p+0, 0x1.56f4736b527dap+0,
-    0x1.5ab07dd485429p+0, 0x1.5e76f15ad2148p+0, 0x1.6247eb03a5585p+0, 0x1.6623882552225p+0,
-    0x1.6a09e667f3bcdp+0, 0x1.6dfb23c651a2fp+0, 0x1.71f75e8ec5f74p+0, 0x1.75feb564267c9p+0,
-    0x1.7a11473eb0187p+0, 0x1.7e2f336cf4e62p+0, 0x1.82589994cce13p+0, 0x1.868d99b4492edp+0,
-    0x1.8ace5422aa0dbp+0, 0x1.8f1ae99157736p+0, 0x1.93737b0cdc5e5p+0, 0x1.97d829fde4e50p+0,
-    0x1.9c49182a3f090p+0, 0x1.a0c667b5de565p+0, 0x1.a5503b23e255dp+0, 0x1.a9e6b5579fdbfp+0,
-    0x1.ae89f995ad3adp+0, 0x1.b33a2b84f15fbp+0, 0x1.b7f76f2fb5e47p+0, 0x1.bcc1e904bc1d2p+0,
-    0x1.c199bdd85529cp+0, 0x1.c67f12e57d14bp+0, 0x1.cb720dcef9069p+0, 0x1.d072d4a07897cp+0,
-    0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
-    0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0};
-
 // ---------------------------------------------------------------------------
 // errors
 static thread_local std::string g_err;
@@ -598,6 +580,31 @@ extern "C" int32_t sas_stage_times(sas_plan* pl, float* ms, int32_t* stage, int3
   }
   return n;
 }
+// Dynamic shared-memory opt-in, once per kernel instantiation and device: the
+// attribute is raised to the device maximum (it is a cap; occupancy and the
+// launch use each call's own size), so concurrent callers never lower it
+// between another thread's set and launch.
+template <auto Kern>
+static int smem_optin(bool carveout_max = true) {
+  static std::mutex m;
+  static uint64_t done = 0;
+  int dev = 0;
+  SAS_CUDA_CHECK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(m);
+  if ((done >> dev) & 1) return SAS_OK;
+  int optin = 0;
+  SAS_CUDA_CHECK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  SAS_CUDA_CHECK(cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  if (carveout_max) SAS_CUDA_CHECK(cudaFuncSetAttribute(Kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  done |= 1ull << dev;
+  return SAS_OK;
+}
+#define SMEM_OPTIN(...)                         \
+  do {                                          \
+    const int _rc = smem_optin<__VA_ARGS__>();  \
+    if (_rc) return _rc;                        \
+  } while (0)
+
 // ---------------------------------------------------------------------------
 // K4 launch: pick (NC, RPT) and the CTA size for (s, r).
 template <typename T, int NC, int RPT, class Asm>
@@ -605,8 +612,7 @@ static int launch_lsq_t(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t
   const int W = (a.s + RPT - 1) / RPT;
   const size_t smem = lsq_smem_bytes<T>(a.s, a.r, W, NC, scratch);
   auto kern = k_lsq<T, NC, RPT, Asm>;
-  SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  SMEM_OPTIN(k_lsq<T, NC, RPT, Asm>);
   int occ = 0;
   SAS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * W, smem));
   if (occ < 1) {
@@ -628,8 +634,7 @@ template <typename T, int RG, int RA, int CB, int W, class Asm>
 static int launch_lsq_mw_t(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t scratch, cudaStream_t st) {
   const size_t smem = lsq_mw_smem_bytes<T>(a.s, a.r, W, (32 / RG) * CB, scratch);
   auto kern = k_lsq_mw<T, RG, RA, CB, W, Asm>;
-  SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  SMEM_OPTIN(k_lsq_mw<T, RG, RA, CB, W, Asm>);
   int occ = 0;
   SAS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * W, smem));
   if (occ < 1) {
@@ -651,8 +656,7 @@ template <int RA, int NCW, int W, int MINB = 1, bool PARK = false, class Asm>
 static int launch_lsq_cw_t(sas_plan* pl, const LsqArgs<double>& a, const Asm& as, size_t scratch, cudaStream_t st) {
   const size_t smem = lsq_cw_smem_bytes(a.s, a.r, RA, scratch, PARK);
   auto kern = k_lsq_cw<RA, NCW, W, Asm, MINB, PARK>;
-  SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  SAS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+  SMEM_OPTIN(k_lsq_cw<RA, NCW, W, Asm, MINB, PARK>);
   int occ = 0;
   SAS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * W, smem));
   if (occ < 1) {
@@ -816,8 +820,9 @@ static int launch_gauss_k(sas_plan* pl, const double* params, int64_t P, double*
   auto kern1 = k_gauss_rows<NT, PW, MINB, MAXW, 1>;
   auto kern2 = k_gauss_rows<NT, PW, MINB, MAXW, 2>;
   const bool two = k3_two_kernels();
-  for (auto kf : {kern0, kern1, kern2})
-    SAS_CUDA_CHECK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SMEM_OPTIN(k_gauss_rows<NT, PW, MINB, MAXW, 0>);
+  SMEM_OPTIN(k_gauss_rows<NT, PW, MINB, MAXW, 1>);
+  SMEM_OPTIN(k_gauss_rows<NT, PW, MINB, MAXW, 2>);
   int occ = 0;
   SAS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, two ? kern1 : kern0, 32 * nw, smem));
   const int64_t nch = pl->n_pad / kGaussKC, ctas = ((P + PW - 1) / PW) * gy;
@@ -1015,8 +1020,8 @@ extern "C" int sas_solve_host(sas_plan* pl, const void* params, int64_t P, const
 static int launch_lift_dmma(sas_plan* pl, const double* coef, int64_t P, double* x, cudaStream_t st,
                             bool blk16 = false) {
   const size_t smem = 2 * (size_t)kLiftNodes * lift_ld(pl->r) * sizeof(double);
-  SAS_CUDA_CHECK(cudaFuncSetAttribute(k_lift_dmma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  SAS_CUDA_CHECK(cudaFuncSetAttribute(k_lift_dmma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (int rc = smem_optin<k_lift_dmma<false>>(false)) return rc;
+  if (int rc = smem_optin<k_lift_dmma<true>>(false)) return rc;
   for (int64_t p0 = 0; p0 < P; p0 += 65535LL * kLiftPar) {
     const int64_t pc = (P - p0 < 65535LL * kLiftPar) ? P - p0 : 65535LL * kLiftPar;
     dim3 grid((unsigned)((pl->n + kLiftNodes - 1) / kLiftNodes), (unsigned)((pc + kLiftPar - 1) / kLiftPar));

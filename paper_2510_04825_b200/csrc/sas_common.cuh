@@ -5,8 +5,9 @@
 //   where bitwise agreement with the reference's affine combine matters
 //   (online.py:108-112).
 // * Scalar traits so the least-squares kernel is one template for f64 and c128.
-// * sas_exp64: table(64)+degree-5 exp for the kernel-row contraction, ~10 FP64
-//   pipe ops instead of the ~24-DFMA-equivalent libdevice exp (measured on B200,
+// * 2048-entry-table FP64 exponentials for the kernel-row contraction (K3) and
+//   the stencil residual checker (K6): 5-9 FP64-pipe ops instead of the
+//   ~24-DFMA-equivalent libdevice exp (measured on B200,
 //   profiles/r01_fp64_peaks.jsonl).
 #pragma once
 #include <cstdint>
@@ -135,103 +136,18 @@ struct Sc<cplx> {
 };
 
 // ---- fast FP64 exp ----------------------------------------------------------
-// e^x = 2^(k/64) * e^r,  k = rint(x*64/ln2),  r = x - k*ln2/64 (two-constant
-// Cody-Waite), |r| <= ln2/128.  e^r - 1 by degree-5 Taylor (truncation
-// r^6/720 <= 3.4e-17).  2^(j/64), j = k mod 64, comes from a 64-entry table held
-// in two registers per lane and fetched with warp shuffles (conflict-free, no
-// shared memory).  2^(k div 64) is applied to the exponent field.  Inputs
-// below -708.39 return 0 (the true value is subnormal, < 2.3e-308); the kernels
-// only evaluate x <= 0.
-// Exact split of ln2/64: hi has its low 20 mantissa bits zero so k*hi is exact
-// for |k| < 2^20; lo = ln2/64 - hi.  Values from mpmath at 50 digits.
-#define SAS_LN2D64_HI 0x1.62e42fef00000p-7
-#define SAS_LN2D64_LO 0x1.473de6af278edp-40
-#define SAS_INVLN2X64 0x1.71547652b82fep+6
 #define SAS_EXP_MAGIC 0x1.8p52
 
-// 2^(j/2048), j = 0..2047 (correctly rounded), copied to shared memory by K3.
+// 2^(j/2048), j = 0..2047 (correctly rounded), copied to shared memory by K3/K6.
 __device__ const double g_exp2_tab2048[2048] = {
 #include "exp2_table2048.inc"
 };
 
-// 2^(j/64), j = 0..63 (correctly rounded; libsas is a single translation unit).
-__constant__ double c_exp2_tab64[64] = {
-    0x1.0000000000000p+0, 0x1.02c9a3e778061p+0, 0x1.059b0d3158574p+0, 0x1.0874518759bc8p+0,
-    0x1.0b5586cf9890fp+0, 0x1.0e3ec32d3d1a2p+0, 0x1.11301d0125b51p+0, 0x1.1429aaea92de0p+0,
-    0x1.172b83c7d517bp+0, 0x1.1a35beb6fcb75p+0, 0x1.1d4873168b9aap+0, 0x1.2063b88628cd6p+0,
-    0x1.2387a6e756238p+0, 0x1.26b4565e27cddp+0, 0x1.29e9df51fdee1p+0, 0x1.2d285a6e4030bp+0,
-    0x1.306fe0a31b715p+0, 0x1.33c08b26416ffp+0, 0x1.371a7373aa9cbp+0, 0x1.3a7db34e59ff7p+0,
-    0x1.3dea64c123422p+0, 0x1.4160a21f72e2ap+0, 0x1.44e086061892dp+0, 0x1.486a2b5c13cd0p+0,
-    0x1.4bfdad5362a27p+0, 0x1.4f9b2769d2ca7p+0, 0x1.5342b569d4f82p+0, 0x1.56f4736b527dap+0,
-    0x1.5ab07dd485429p+0, 0x1.5e76f15ad2148p+0, 0x1.6247eb03a5585p+0, 0x1.6623882552225p+0,
-    0x1.6a09e667f3bcdp+0, 0x1.6dfb23c651a2fp+0, 0x1.71f75e8ec5f74p+0, 0x1.75feb564267c9p+0,
-    0x1.7a11473eb0187p+0, 0x1.7e2f336cf4e62p+0, 0x1.82589994cce13p+0, 0x1.868d99b4492edp+0,
-    0x1.8ace5422aa0dbp+0, 0x1.8f1ae99157736p+0, 0x1.93737b0cdc5e5p+0, 0x1.97d829fde4e50p+0,
-    0x1.9c49182a3f090p+0, 0x1.a0c667b5de565p+0, 0x1.a5503b23e255dp+0, 0x1.a9e6b5579fdbfp+0,
-    0x1.ae89f995ad3adp+0, 0x1.b33a2b84f15fbp+0, 0x1.b7f76f2fb5e47p+0, 0x1.bcc1e904bc1d2p+0,
-    0x1.c199bdd85529cp+0, 0x1.c67f12e57d14bp+0, 0x1.cb720dcef9069p+0, 0x1.d072d4a07897cp+0,
-    0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
-    0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0};
-
-
-// Per-lane table registers: lo = 2^(lane/64), hi = 2^((lane+32)/64).
-struct ExpTab {
-  double lo, hi;
-};
-
-__device__ __forceinline__ ExpTab exp_tab_load(int lane) {
-  return ExpTab{c_exp2_tab64[lane], c_exp2_tab64[lane + 32]};
-}
-
-// Shared pieces of the exp: range reduction + polynomial, and the final scaling.
-// Returns q = e^r - 1 and k.
-__device__ __forceinline__ double sas_exp64_core(double x, int& ki) {
-  double kd = fma(x, SAS_INVLN2X64, SAS_EXP_MAGIC);
-  ki = __double2loint(kd);
-  double kf = kd - SAS_EXP_MAGIC;
-  double r = fma(-kf, SAS_LN2D64_HI, x);
-  r = fma(-kf, SAS_LN2D64_LO, r);
-  // e^r - 1 = r (1 + r/2 + r^2/6 + r^3/24 + r^4/120)
-  double q = fma(r, 1.0 / 120.0, 1.0 / 24.0);
-  q = fma(q, r, 1.0 / 6.0);
-  q = fma(q, r, 0.5);
-  q = fma(q, r, 1.0);
-  return q * r;
-}
-
-// res = t (1 + q) scaled by 2^(k div 64); k < -65407 (x < -708.39, true value
-// subnormal) flushes to +0 with integer ops only (no FP64-pipe compare).
-__device__ __forceinline__ double sas_exp64_finish(double t, double q, int ki) {
-  double res = fma(t, q, t);  // in [0.99, 2.01)
-  int e = ki >> 6;            // floor(k / 64)
-  int hi = __double2hiint(res) + (e << 20);
-  int lo = __double2loint(res);
-  const int keep = (ki >= -65407) ? -1 : 0;
-  return __hiloint2double(hi & keep, lo & keep);
-}
-
-// All 32 lanes of the warp must call this together (warp shuffles).
-__device__ __forceinline__ double sas_exp64(double x, const ExpTab& tab) {
-  int ki;
-  const double q = sas_exp64_core(x, ki);
-  const int j = ki & 63;
-  const double tlo = __shfl_sync(0xffffffffu, tab.lo, j & 31);
-  const double thi = __shfl_sync(0xffffffffu, tab.hi, j & 31);
-  return sas_exp64_finish((j & 32) ? thi : tlo, q, ki);
-}
-
-// Same algorithm with the 2^(j/64) table in shared memory (no warp collectives).
-__device__ __forceinline__ double sas_exp64_smem(double x, const double* __restrict__ tab_s) {
-  int ki;
-  const double q = sas_exp64_core(x, ki);
-  return sas_exp64_finish(tab_s[ki & 63], q, ki);
-}
-
-// K3 variant: 2048-entry table in shared memory, degree-3 polynomial.
+// General form (K6 stencil checker): 2048-entry table in shared memory, degree-3 polynomial.
 //   k = rint(x 2048/ln2), r = x - k ln2/2048 (two-constant, |r| <= ln2/4096),
 //   e^r - 1 = r (1 + r/2 + r^2/6) (truncation r^4/24 <= 3.4e-17),
 //   e^x = 2^(k mod 2048 / 2048) (1 + q) 2^(k div 2048).
-// 9 FP64-pipe ops per value (the 64-entry version needs 11).  k < -2093055
+// 9 FP64-pipe ops per value.  k < -2093055
 // (x < -708.39) flushes to +0.
 #define SAS_INVLN2X2K 0x1.71547652b82fep+11
 #define SAS_LN2D2K_HI 0x1.62e42fec00000p-12

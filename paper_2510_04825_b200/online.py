@@ -36,7 +36,7 @@ from . import _capi
 from .errors import BackendError, RankDeficiencyError
 from .systems import GaussianKernelOperator, StencilOperator
 
-PLAN_CHECK_RTOL = 1e-13
+PLAN_CHECK_RTOL = 1e-10   # online.py:93 (affine blocks vs the row oracle)
 
 
 # --------------------------------------------------------------------------
@@ -61,6 +61,37 @@ def params_to_array(parameters, dp: int, pcomplex: bool) -> np.ndarray:
     return np.ascontiguousarray(arr.real)
 
 
+def is_cuda_tensor(a) -> bool:
+    return hasattr(a, "data_ptr") and getattr(a, "is_cuda", False)
+
+
+def row_operator(system):
+    """The GPU row operator of a non-affine system: our `operator` attribute,
+    or, for the reference's own KRR system (systems.py:423-463: row_fn =
+    _kernels.rbf_rows over the 1-D training points, p = (lambda, sigma)), the
+    equivalent Gaussian-kernel descriptor."""
+    op = getattr(system, "operator", None)
+    if op is not None:
+        return op
+    ex = getattr(system, "extras", None) or {}
+    if getattr(system, "name", "") == "krr" and "t_train" in ex and system.affine_terms is None:
+        pts = np.ascontiguousarray(np.asarray(ex["t_train"], dtype=np.float64).reshape(-1, 1))
+        return GaussianKernelOperator(points=pts, ridge=0.0, ridge_from_param=True)
+    return None
+
+
+def probe_point(system, basis=None):
+    """A parameter value inside the system's domain: the basis' first snapshot
+    point (the point the reference's plan spot check uses, online.py:87), else
+    the domain's lower corner."""
+    pts = getattr(basis, "points", None)
+    if pts is not None and len(pts):
+        return pts[0]
+    axes = system.domain.axes
+    vals = [(1j * a.lo if a.imag else a.lo) for a in axes]
+    return vals[0] if len(vals) == 1 else tuple(vals)
+
+
 class GpuPlan:
     """libsas plan for one (system, basis, selector) on one CUDA device."""
 
@@ -69,14 +100,16 @@ class GpuPlan:
         self.lib = _capi.load()
         self.system = system
         self.device = int(device)
-        X = np.asarray(basis.basis)
+        Xb = basis.basis
+        self.x_device = is_cuda_tensor(Xb)
+        X = Xb if self.x_device else np.asarray(Xb)
         self.n, self.r = X.shape
         idx = np.ascontiguousarray(selector.indices, dtype=np.int64)
         self.s = idx.size
         self.dp = int(system.domain.dim) if hasattr(system, "domain") else 1
         self.pcomplex = bool(getattr(system.domain, "axes", None) and any(a.imag for a in system.domain.axes))
         terms = system.affine_terms
-        complex_data = (np.iscomplexobj(X) or force_complex or self.pcomplex
+        complex_data = ((X.is_complex() if self.x_device else np.iscomplexobj(X)) or force_complex or self.pcomplex
                         or (blocks is not None and any(np.iscomplexobj(b) for b in blocks))
                         or (proj is not None and np.iscomplexobj(proj)))
         if terms is not None:
@@ -89,6 +122,18 @@ class GpuPlan:
             self.rhs_constant = False
         if self.rhs_constant and np.iscomplexobj(system.b):
             complex_data = True
+        # opaque callables (kind "other" coefficients, rhs_fn) are evaluated on the
+        # host per parameter; probe them once at a domain point so a complex value
+        # on a real-parameter domain selects a complex plan (the reference computes
+        # such systems in complex128, online.py:108-117)
+        if not complex_data:
+            p0 = probe_point(system, basis)
+            if terms is not None:
+                for t in terms:
+                    if getattr(t, "kind", "other") not in _KIND_CODES and complex(t.coeff(p0)).imag != 0.0:
+                        complex_data = True
+            if not self.rhs_constant and np.iscomplexobj(np.asarray(system.rhs(p0, idx[:1]))):
+                complex_data = True
         self.complex = bool(complex_data)
         self.np_dtype = np.complex128 if self.complex else np.float64
         # the reference coerces const/linear coefficients to complex (systems.py:92, 98):
@@ -103,7 +148,7 @@ class GpuPlan:
         desc.param_complex = 1 if self.pcomplex else 0
         keep = []  # keep host arrays alive during the call
         self.table_terms = []
-        op = getattr(system, "operator", None)
+        op = row_operator(system)
         if terms is not None:
             K = len(terms)
             kinds = np.zeros(K, dtype=np.int32)
@@ -149,7 +194,15 @@ class GpuPlan:
         else:
             raise ValueError("system has neither affine terms nor a GPU row operator")
 
-        Xc = np.ascontiguousarray(X.astype(self.np_dtype, copy=False))
+        flags = 0
+        if self.x_device:  # e.g. the NCCL-broadcast basis: no host round trip
+            import torch
+            Xc = X.to(device=f"cuda:{self.device}",
+                      dtype=torch.complex128 if self.complex else torch.float64).contiguous()
+            flags |= _capi.SAS_FLAG_INPUT_DEVICE
+            torch.cuda.synchronize(self.device)
+        else:
+            Xc = np.ascontiguousarray(X.astype(self.np_dtype, copy=False))
         w = None if selector.weights is None else np.ascontiguousarray(selector.weights, dtype=np.float64)
         if self.rhs_constant:
             t = np.ascontiguousarray(np.asarray(system.b)[idx].astype(self.np_dtype))
@@ -161,7 +214,7 @@ class GpuPlan:
         rc = self.lib.sas_plan_create(C.byref(desc), _capi.ptr(Xc), self.n, self.r,
                                       idx.ctypes.data_as(C.POINTER(C.c_int64)),
                                       None if w is None else w.ctypes.data_as(C.POINTER(C.c_double)),
-                                      self.s, _capi.ptr(t), _capi.ptr(pj), self.device, 0, C.byref(handle))
+                                      self.s, _capi.ptr(t), _capi.ptr(pj), self.device, flags, C.byref(handle))
         _capi.check(rc, "sas_plan_create")
         self.handle = handle
         self.has_proj = proj is not None
@@ -179,14 +232,18 @@ class GpuPlan:
         for i, p in enumerate(parameters):
             for k in self.table_terms:
                 v = complex(self.system.affine_terms[k].coeff(p))
+                if v.imag != 0.0 and not self.complex:
+                    raise ValueError(f"affine term {k} has a complex coefficient at p={p} on a real plan")
                 tab[i, k] = (v.real, v.imag)
         return tab
 
     def rhs_table(self, parameters) -> Optional[np.ndarray]:
         if self.rhs_constant:
             return None
-        return np.ascontiguousarray(np.stack([np.asarray(self.system.rhs(p, self.indices)) for p in parameters])
-                                    .astype(self.np_dtype))
+        rows = np.stack([np.asarray(self.system.rhs(p, self.indices)) for p in parameters])
+        if not self.complex and np.iscomplexobj(rows) and np.any(rows.imag != 0):
+            raise ValueError("complex right-hand side on a real plan")
+        return np.ascontiguousarray(rows.astype(self.np_dtype))
 
     # -- calls -----------------------------------------------------------------
     def solve_host(self, parameters):
@@ -262,10 +319,9 @@ class OnlineSolution:
     def lift(self) -> np.ndarray:
         """x = Q_X c, computed on the GPU (libsas sas_lift), cached."""
         if self._lifted is None:
-            if self._plan is not None and self._plan.gpu is not None:
-                self._lifted = lift_batch(self._plan, self.coefficients[None, :])[0]
-            else:
-                self._lifted = self._basis.basis @ self.coefficients
+            if self._plan is None:
+                raise BackendError("solution has no device plan to lift with")
+            self._lifted = lift_batch(self._plan, self.coefficients[None, :])[0]
         return self._lifted
 
 
@@ -293,20 +349,71 @@ class BatchResult:
 
 
 # --------------------------------------------------------------------------
+def _rows_times_basis(m, X):
+    """(sparse rows m) @ X for a host array X, or for a CUDA tensor X by
+    gathering only the rows of X that m touches (same entries in the same
+    stored order, so the products match m @ X_host)."""
+    import scipy.sparse as sp
+    m = sp.csr_matrix(m)
+    if not is_cuda_tensor(X):
+        return np.asarray(m @ X)
+    import torch
+    cols = np.unique(m.indices)
+    xs = X[torch.from_numpy(cols).to(X.device)].cpu().numpy()
+    sub = sp.csr_matrix((m.data, np.searchsorted(cols, m.indices), m.indptr), shape=(m.shape[0], cols.size))
+    return np.asarray(sub @ xs)
+
+
+def _spot_check(system, basis, idx, uniq, inverse, blocks):
+    """The reference's plan check (online.py:86-96): at basis.points[0] the
+    combined affine blocks must match a direct row-oracle assembly to 1e-10
+    relative, else RankDeficiencyError.  The direct rows come from the
+    system's own row oracle when it has one (reference ParametricSystem.rows,
+    systems.py:134-149), else from the affine terms row by row."""
+    p0 = probe_point(system, basis)
+    if hasattr(system, "rows"):
+        rows = system.rows(p0, uniq)
+    else:
+        rows = None
+        for term in system.affine_terms:
+            blk = term.matrix[uniq] * term.coeff(p0)
+            rows = blk if rows is None else rows + blk
+    direct = _rows_times_basis(rows, basis.basis)[inverse]
+    combined = sum(term.coeff(p0) * blk for term, blk in zip(system.affine_terms, blocks))
+    err = np.linalg.norm(combined - direct)
+    ref = max(np.linalg.norm(direct), 1e-300)
+    if err > PLAN_CHECK_RTOL * ref:
+        raise RankDeficiencyError(f"affine blocks disagree with row oracle (rel err {err / ref:.2e})")
+
+
 def precompute_online(system, basis, selector, device: int = 0) -> OnlinePlan:
     """Precompute the selector-row blocks of each affine term (host, as the
-    reference does, online.py:77-85) and build the device plan."""
+    reference does, online.py:77-85), run the reference's spot check
+    (online.py:86-96) and build the device plan.  `basis.basis` may be a host
+    array or a CUDA tensor (e.g. the NCCL-broadcast basis, parallel.py); only
+    the rows the blocks touch are then read back."""
     if basis.n != system.n or selector.n != system.n:
         raise ValueError("system/basis/selector dimension mismatch")
     idx = np.asarray(selector.indices, dtype=np.int64)
     uniq, inverse = np.unique(idx, return_inverse=True)
-    sampled_basis = np.asarray(basis.basis)[idx]
+    X = basis.basis
+    if is_cuda_tensor(X):
+        import torch
+        sampled_basis = X[torch.from_numpy(idx).to(X.device)].cpu().numpy()
+    else:
+        sampled_basis = np.asarray(X)[idx]
     blocks = None
     if system.affine_terms is not None:
-        blocks = tuple(np.asarray(term.matrix[uniq] @ basis.basis)[inverse] for term in system.affine_terms)
+        blocks = tuple(_rows_times_basis(term.matrix[uniq], X)[inverse] for term in system.affine_terms)
+        _spot_check(system, basis, idx, uniq, inverse, blocks)
     proj = None
     if system.output_functional is not None:
-        proj = system.output_functional.conj() @ basis.basis
+        if is_cuda_tensor(X):
+            import torch
+            c = torch.from_numpy(np.ascontiguousarray(np.asarray(system.output_functional).conj())).to(X.device)
+            proj = (c.to(torch.promote_types(c.dtype, X.dtype)) @ X.to(torch.promote_types(c.dtype, X.dtype))).cpu().numpy()
+        else:
+            proj = system.output_functional.conj() @ X
     gpu = GpuPlan(system, basis, selector, blocks, proj, device=device)
     return OnlinePlan(system=system, basis=basis, selector=selector, blocks=blocks,
                       sampled_basis=sampled_basis, output_projection=proj, gpu=gpu)
@@ -407,7 +514,9 @@ def _operator_times_basis(system, X, p, dev):
     import torch
     op = getattr(system, "operator", None)
     if system.affine_terms is not None:
-        cdt = torch.complex128 if X.is_complex() or np.iscomplexobj(p) else torch.float64
+        fs = [complex(t.coeff(p)) for t in system.affine_terms]
+        cplx_ = X.is_complex() or np.iscomplexobj(p) or any(f.imag != 0.0 for f in fs)
+        cdt = torch.complex128 if cplx_ else torch.float64
         B = torch.zeros(X.shape, dtype=cdt, device=dev)
         for t in system.affine_terms:
             m = t.matrix.tocsr()
@@ -418,7 +527,7 @@ def _operator_times_basis(system, X, p, dev):
                                             torch.from_numpy(m.data.astype(np.complex128 if cdt == torch.complex128
                                                                            else np.float64)),
                                             size=m.shape, device=dev, check_invariants=True)
-            f = complex(t.coeff(p))
+            f = fs[system.affine_terms.index(t)]
             B += (f if cdt == torch.complex128 else f.real) * (A @ X.to(cdt))
         return B
     if isinstance(op, StencilOperator):
@@ -459,7 +568,12 @@ def solve_apsnap(system, basis, p, device: int = 0):
     dev = torch.device(f"cuda:{device}")
     X = torch.from_numpy(np.ascontiguousarray(basis.basis)).to(dev)
     B = _operator_times_basis(system, X, p, dev)
-    rhs = torch.from_numpy(np.ascontiguousarray(np.asarray(system.full_rhs(p)))).to(dev).to(B.dtype)
+    rhs = torch.from_numpy(np.ascontiguousarray(np.asarray(system.full_rhs(p)))).to(dev)
+    if rhs.is_complex() and not B.is_complex():
+        B = B.to(torch.complex128)
+    rhs = rhs.to(B.dtype)
+    if not bool(torch.isfinite(B).all()):
+        raise ValueError("matrix has non-finite entries")   # linalg._as_matrix, linalg.py:36-37
     q, rmat = torch.linalg.qr(B, mode="reduced")
     diag = rmat.diagonal().abs()
     if diag.numel() and float(diag.min()) < 1e-12 * max(float(diag.max()), np.finfo(float).tiny):
