@@ -55,9 +55,13 @@ def _device_for(backend: str, local_rank: int):
     return torch.device(f"cuda:{local_rank}") if backend == "nccl" else torch.device("cpu")
 
 
-def broadcast_inputs(arrays: dict, src: int = 0, local_rank: int = 0) -> dict:
+def broadcast_inputs(arrays: dict, src: int = 0, local_rank: int = 0, device_keys=()) -> dict:
     """Broadcast a dict of numpy arrays from `src` to all ranks (shapes/dtypes
-    first as an object, then one tensor broadcast per array)."""
+    first as an object, then one tensor broadcast per array).  Under NCCL the
+    arrays named in `device_keys` (e.g. the basis X) are returned as CUDA
+    tensors on this rank's device -- the plan consumes them in place
+    (SAS_FLAG_INPUT_DEVICE), with no device->host->device round trip; every
+    other array comes back as numpy."""
     import torch
     import torch.distributed as dist
     backend = dist.get_backend()
@@ -78,7 +82,11 @@ def broadcast_inputs(arrays: dict, src: int = 0, local_rank: int = 0) -> dict:
         else:
             t = torch.empty(int(np.prod(shape)) * npdt.itemsize, dtype=torch.uint8, device=dev)
         dist.broadcast(t, src=src)
-        out[key] = t.cpu().numpy().view(npdt).reshape(shape)
+        if key in device_keys and t.is_cuda:
+            tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.complex128): torch.complex128}[npdt]
+            out[key] = t.view(tdt).reshape(shape)
+        else:
+            out[key] = t.cpu().numpy().view(npdt).reshape(shape)
     return out
 
 
