@@ -143,8 +143,12 @@ def ls_floor(m, tb, weights, draws=4, seed=0, rows=None, basis=None, inverse=Non
     eps = np.finfo(float).eps
     for _ in range(draws):
         dt = 1.0 + eps * rng.choice([-1.0, 1.0], size=tb.shape)
-        if rows is not None:
-            rr = np.asarray(rows.toarray() if hasattr(rows, "toarray") else rows)
+        if rows is not None and hasattr(rows, "tocsr"):  # sparse rows: perturb the stored entries
+            rr = rows.tocsr(copy=True)
+            rr.data = rr.data * (1.0 + eps * rng.choice([-1.0, 1.0], size=rr.data.shape))
+            mp = np.asarray(rr @ basis)[inverse]
+        elif rows is not None:
+            rr = np.asarray(rows)
             dr = 1.0 + eps * rng.choice([-1.0, 1.0], size=rr.shape)
             mp = np.asarray((rr * dr) @ basis)[inverse]
         else:

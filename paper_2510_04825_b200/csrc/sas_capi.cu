@@ -776,20 +776,17 @@ static int launch_lsq(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t s
 // (gauss_pw), 2 CTAs/SM, split-K chosen against the wave count.  Tuning:
 // SAS_K3_VARIANT=<pw>,<minb> for 17 <= r <= 24 (NT == 3), SAS_K3_KSPLIT,
 // SAS_K3_MAXW.
-// Split-K factor: the smallest z in 1..kGaussMaxSplit minimising the wave
-// count ceil(ctas z / slots) / z (a partial last wave of whole-n CTAs costs up
-// to a full wave); SAS_K3_KSPLIT forces it.
-static int gauss_ksplit(int64_t ctas, int64_t slots, int64_t nchunks) {
+// Split-K factor: a plan property, not a function of P, so every parameter
+// value's M (and hence its coefficients) is bitwise the same whatever batch or
+// shard it is solved in: kGaussMaxSplit whenever the n chunks allow it (2 halves
+// of n; measured against the wave count on config 2: 2048 CTAs on 296 slots
+// leave a 92 % last wave instead of 46 %).  SAS_K3_KSPLIT forces it.
+static int gauss_ksplit(int64_t nchunks) {
   const char* e = getenv("SAS_K3_KSPLIT");
   if (e) return std::max(1, std::min(kGaussMaxSplit, atoi(e)));
-  int best = 1;
-  double bt = 1e300;
-  for (int z = 1; z <= kGaussMaxSplit; ++z) {
-    if (nchunks < (int64_t)z * kG3Stages) break;
-    const double t = (double)((ctas * z + slots - 1) / slots) / z;
-    if (t < bt - 1e-9) { bt = t; best = z; }
-  }
-  return best;
+  int z = kGaussMaxSplit;
+  while (z > 1 && nchunks < (int64_t)z * kG3Stages) --z;
+  return z;
 }
 
 // The fast and the masked CTAs run in two launches over the same grid (each
@@ -823,10 +820,8 @@ static int launch_gauss_k(sas_plan* pl, const double* params, int64_t P, double*
   SMEM_OPTIN(k_gauss_rows<NT, PW, MINB, MAXW, 0>);
   SMEM_OPTIN(k_gauss_rows<NT, PW, MINB, MAXW, 1>);
   SMEM_OPTIN(k_gauss_rows<NT, PW, MINB, MAXW, 2>);
-  int occ = 0;
-  SAS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, two ? kern1 : kern0, 32 * nw, smem));
-  const int64_t nch = pl->n_pad / kGaussKC, ctas = ((P + PW - 1) / PW) * gy;
-  const int z = gauss_ksplit(ctas, (int64_t)std::max(occ, 1) * pl->sms, nch);
+  const int64_t nch = pl->n_pad / kGaussKC;
+  const int z = gauss_ksplit(nch);
   *ksplit = z;
   dim3 grid((unsigned)((P + PW - 1) / PW), (unsigned)gy, (unsigned)z);
   stage_begin(pl, st, SAS_STAGE_GAUSS_ROWS);
