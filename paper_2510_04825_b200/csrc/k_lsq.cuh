@@ -20,7 +20,9 @@
 // GPU count).  Two __syncthreads per column step; column k and row k are
 // double-buffered.
 //
-// The assembler functor fills Ms with the unweighted M(p):
+// The assembler functor fills Ms with the unweighted M(p), entry (i, j) at
+// Ms[i * ldm + j * ldc] (ldc = 1: row-major; k_lsq_sm passes ldm = 1 and
+// ldc = its column stride for a column-major matrix):
 //   AsmGlobal  - M precomputed by another kernel (Gaussian kernel rows, K3)
 //   AsmAffine  - M = sum_k f_k(p) B_k with numpy's operation order (K1)
 //   AsmStencil - edge-form stencil rows with exp-affine coefficients (K2)
@@ -96,7 +98,7 @@ struct AsmGlobal {
   static constexpr size_t scratch_bytes(int, int) { return 0; }
   template <class Grp>
   __device__ __forceinline__ void operator()(const Grp& g, int64_t p, T* Ms, int ldm, int s, int r,
-                                             unsigned char*) const {
+                                             unsigned char*, int ldc = 1) const {
     const T* src = M + p * (int64_t)s * r;
     RowMajorWalk wk(g.rank(), g.size(), r);
     if (nsplit == 2) {  // K3's split-K partials: loads of 4 entries issued before their adds
@@ -112,7 +114,7 @@ struct AsmGlobal {
         }
 #pragma unroll
         for (int t = 0; t < U; ++t) {
-          if (base + t * step < total) Ms[wk.i * ldm + wk.j] = v0[t] + v1[t];
+          if (base + t * step < total) Ms[wk.i * ldm + wk.j * ldc] = v0[t] + v1[t];
           wk.next();
         }
       }
@@ -121,7 +123,7 @@ struct AsmGlobal {
     for (int idx = g.rank(); idx < s * r; idx += g.size(), wk.next()) {
       T v = src[idx];
       for (int z = 1; z < nsplit; ++z) v = v + src[idx + z * split];
-      Ms[wk.i * ldm + wk.j] = v;
+      Ms[wk.i * ldm + wk.j * ldc] = v;
     }
   }
 };
@@ -175,7 +177,7 @@ struct AsmAffine {
   static constexpr size_t scratch_bytes(int, int) { return 16 * sizeof(T); }
   template <class Grp>
   __device__ __forceinline__ void operator()(const Grp& g, int64_t p, T* Ms, int ldm, int s, int r,
-                                             unsigned char* scratch) const {
+                                             unsigned char* scratch, int ldc = 1) const {
     T* f = reinterpret_cast<T*>(scratch);
     if (g.rank() < K) {
       int k = g.rank();
@@ -191,7 +193,7 @@ struct AsmAffine {
       // m = f0*B0; m = m + fk*Bk  (online.py:110-112, numpy elementwise order)
       T m = Sc<T>::mul_exact(f[0], blocks[idx]);
       for (int k = 1; k < K; ++k) m = Sc<T>::add_exact(m, Sc<T>::mul_exact(f[k], blocks[k * blk + idx]));
-      Ms[wk.i * ldm + wk.j] = m;
+      Ms[wk.i * ldm + wk.j * ldc] = m;
     }
   }
 };
@@ -203,7 +205,12 @@ struct AsmAffine {
 // with X accumulates the row's nonzeros in ascending column order with FMA,
 // as the reference's dense rows_dense(...) @ basis does (online.py:62):
 //   G[i][q] = X[node_q], gmap[i][q] = 0 (diagonal) | 1+e (edge e) | -1 (pad).
-struct AsmStencil {
+// kRows = 0: one (row, column) entry per thread, kUnroll entries' gathered
+// rows in flight; kRows >= 1: one warp per selected row, kRows rows at a time,
+// every lane owns column pairs (2 lane + 64 m, +1) loaded as 16-byte vectors
+// (all E+1 gathered rows of kRows rows in flight per lane).  Same FMA order.
+template <int kUnroll = 4, int kRows = 0>
+struct AsmStencilT {
   static constexpr int kMaxEdges = 7;  // E + 1 <= 8 gathered rows per selected row
   int E, dp;
   const double* phi;    // s x E x dp
@@ -216,7 +223,7 @@ struct AsmStencil {
   static size_t scratch_bytes(int s, int) { return (size_t)s * 8 * sizeof(double); }
   template <class Grp>
   __device__ __forceinline__ void operator()(const Grp& g, int64_t p, double* Ms, int ldm, int s, int r,
-                                             unsigned char* scratch) const {
+                                             unsigned char* scratch, int ldc = 1) const {
     double* cs = reinterpret_cast<double*>(scratch);
     const double* pp = params + p * dp;
     const int E1 = E + 1;
@@ -253,7 +260,43 @@ struct AsmStencil {
     // M = rows @ G in ascending column order with FMA (padding slots add
     // 0 * 0); the gathered rows are L2-resident, the loads of kUnroll entries
     // are issued before their FMA chains
-    constexpr int kUnroll = 4;
+    if constexpr (kRows > 0) {
+      if ((r & 1) == 0) {
+        const int warp = g.rank() >> 5, lane = g.rank() & 31, nw = g.size() >> 5;
+        for (int i0 = warp * kRows; i0 < s; i0 += nw * kRows) {
+          for (int jb = 2 * lane; jb < r; jb += 64) {
+            double2 gv[kRows][8];
+#pragma unroll
+            for (int t = 0; t < kRows; ++t) {
+              const int i = i0 + t;
+              const double* gr = G + ((int64_t)i * E1) * r + jb;
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                gv[t][q] = (i < s && q < E1) ? __ldg(reinterpret_cast<const double2*>(gr + (int64_t)q * r))
+                                             : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int t = 0; t < kRows; ++t) {
+              const int i = i0 + t;
+              if (i >= s) break;
+              const double* ci = cs + i * 8;
+              double mx = 0.0, my = 0.0;
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                if (q < E1) {
+                  const double c = ci[q];
+                  mx = fma(c, gv[t][q].x, mx);
+                  my = fma(c, gv[t][q].y, my);
+                }
+              }
+              Ms[i * ldm + jb * ldc] = mx;
+              Ms[i * ldm + (jb + 1) * ldc] = my;
+            }
+          }
+        }
+        return;
+      }
+    }
     const int total = s * r;
     RowMajorWalk wk(g.rank(), g.size(), r);
     for (int base = g.rank(); base < total; base += kUnroll * g.size()) {
@@ -280,12 +323,13 @@ struct AsmStencil {
             if (2 * q2 < E1) m = fma(a.x, gv[t][2 * q2], m);
             if (2 * q2 + 1 < E1) m = fma(a.y, gv[t][2 * q2 + 1], m);
           }
-          Ms[ii[t] * ldm + jj[t]] = m;
+          Ms[ii[t] * ldm + jj[t] * ldc] = m;
         }
       }
     }
   }
 };
+using AsmStencil = AsmStencilT<4, 2>;
 
 // ---------------------------------------------------------------------------
 template <typename T>

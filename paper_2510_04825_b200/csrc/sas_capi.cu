@@ -19,6 +19,7 @@
 #include "k_lsq.cuh"
 #include "k_lsq_mw.cuh"
 #include "k_lsq_cw.cuh"
+#include "k_lsq_sm.cuh"
 #include "k_gauss.cuh"
 #include "k_recon.cuh"
 
@@ -680,6 +681,69 @@ static int launch_lsq_cw_t(sas_plan* pl, const LsqArgs<double>& a, const Asm& as
   return SAS_OK;
 }
 
+// Shared-memory-resident Householder (k_lsq_sm): one CTA of W warps per
+// parameter value, [W M | W t] column-major in shared memory, MINB CTAs per SM.
+template <typename T, int RA, int W, int MINB, class Asm>
+static int launch_lsq_sm_t(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t scratch, cudaStream_t st) {
+  const size_t smem = lsq_sm_smem_bytes<T>(RA, a.r, scratch);
+  auto kern = k_lsq_sm<T, RA, W, Asm, MINB>;
+  SMEM_OPTIN(k_lsq_sm<T, RA, W, Asm, MINB>);
+  int occ = 0;
+  SAS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * W, smem));
+  if (occ < 1) {
+    sas_set_error("least-squares kernel does not fit (s=%d r=%d smem=%zu)", a.s, a.r, smem);
+    return SAS_ERR_ARG;
+  }
+  int64_t grid = (int64_t)occ * pl->sms;
+  if (grid > a.P) grid = a.P;
+  if (grid < 1) grid = 1;
+  const int rc = ensure(&pl->cw_mg, &pl->cw_mg_n, grid * a.s * (int64_t)(a.r + 1) * (int64_t)sizeof(T));
+  if (rc) return rc;
+  stage_begin(pl, st, SAS_STAGE_LSQ);
+  kern<<<(unsigned)grid, 32 * W, smem, st>>>(a, as, reinterpret_cast<T*>(pl->cw_mg));
+  stage_end(pl, st);
+  SAS_CUDA_CHECK(cudaGetLastError());
+  pl->last_launches++;
+  return SAS_OK;
+}
+
+// SAS_LSQ_SM: "off" never, "1" whenever a variant fits, unset = the default
+// shapes: complex with r+1 >= 16 (config 4, 120 x 31: 17.2 ms vs 19.5 ms for
+// k_lsq_mw per 100,000 p).  For the real large shapes the register-resident
+// column-owner kernel stays ahead (config 5: 45.4 vs 37.1 ms; config 3: 12.6
+// vs 11.1 ms): the shared-memory variant is bound by its per-step column
+// loads/stores (~1.4 K wavefronts per step, profiles/r02_k4_tuning.txt).
+static int lsq_sm_env() {
+  static int v = -3;
+  if (v == -3) {
+    const char* e = getenv("SAS_LSQ_SM");
+    v = !e ? -1 : (strcmp(e, "off") == 0 ? 0 : 1);
+  }
+  return v;
+}
+// returns -1 when no shared-memory variant applies
+template <typename T, class Asm>
+static int try_lsq_sm(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t scratch, cudaStream_t st) {
+  const int env = lsq_sm_env();
+  if (env == 0) return -1;
+  if (env == -1 && std::is_same<T, double>::value) return -1;
+  const int cols = a.r + 1, s = a.s;
+  if (cols < 16 || cols > 64) return -1;
+  if constexpr (std::is_same<Asm, AsmStencil>::value) {
+    // 2 entries' gathered rows in flight instead of 4: no spills under the
+    // 12-16-warp register budget
+    const AsmStencilT<2, 1> as2{as.E, as.dp, as.phi, as.G, as.gmap, as.hh, as.params};
+    return try_lsq_sm<T>(pl, a, as2, scratch, st);
+  } else if constexpr (std::is_same<T, double>::value) {
+    if (s <= 128) return launch_lsq_sm_t<T, 4, 8, 3>(pl, a, as, scratch, st);
+    if (s <= 160) return launch_lsq_sm_t<T, 5, 10, 3>(pl, a, as, scratch, st);
+    if (s <= 224) return launch_lsq_sm_t<T, 7, 12, 2>(pl, a, as, scratch, st);
+  } else {
+    if (s <= 128) return launch_lsq_sm_t<T, 4, 8, 3>(pl, a, as, scratch, st);
+  }
+  return -1;
+}
+
 // Column-owner variants (rows <= 32*RA, columns <= NCW*W) for real shapes
 // with r+1 > 32, in preference order (config 3: {5,7,6} 5.94 ms vs 6.84 ms
 // for k_lsq_mw, 32,768 p; config 5: {7,9,6} with M parked in L2 runs two
@@ -743,6 +807,10 @@ template <typename T, class Asm>
 static int launch_lsq(sas_plan* pl, const LsqArgs<T>& a, const Asm& as, size_t scratch, cudaStream_t st) {
   const int cols = a.r + 1, s = a.s;
   if (!lsq_force_cta()) {
+    {
+      const int rc = try_lsq_sm<T>(pl, a, as, scratch, st);
+      if (rc >= 0) return rc;
+    }
     if constexpr (std::is_same<T, double>::value) {
       const int rc = try_lsq_cw(pl, a, as, scratch, st);
       if (rc >= 0) return rc;

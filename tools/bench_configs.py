@@ -100,7 +100,7 @@ def run(cfg, steps, dev, synthetic=False, P=None, check=True, resid_count=0):
     t0 = time.perf_counter()
     prob = problems.build(cfg)
     if synthetic and cfg != 2:
-        r = {1: 8, 3: 40, 4: 8, 5: 50}[cfg]
+        r = {1: 8, 3: 40, 4: 30, 5: 50}[cfg]   # the real bases: r' = 8, 40, 30, 50
         basis, sel = synthetic_basis(prob, r, complex_=(cfg == 4), device=dev)
         src = f"synthetic orthonormal basis r={r}"
     elif cfg in (1, 2):
