@@ -176,6 +176,16 @@ int32_t sas_last_launch_count(const sas_plan* plan);
 int sas_plan_set_timing(sas_plan* plan, int32_t enable);
 int32_t sas_stage_times(sas_plan* plan, float* ms, int32_t* stage, int32_t cap);
 
+/* R factor of a tall m x w matrix (w <= 64) by TSQR (block Householder QRs,
+ * then the stacked R blocks): the QR of the full least squares
+ * online.solve_apsnap (online.py:156-165 -> linalg.solve_ls, linalg.py:89-113)
+ * and of the leverage selector's range basis (subsample.py:144-159).
+ *   A  m x w row-major, device, dtype SAS_F64 / SAS_C128
+ *   R  w x w row-major, device, upper triangular (np.linalg.qr's R up to
+ *      the signs of its rows)
+ * Stream-ordered; scratch comes from the stream-ordered allocator. */
+int sas_tsqr_r(const void* A, int64_t m, int32_t w, int32_t dtype, void* R, int32_t device, void* stream);
+
 void sas_plan_destroy(sas_plan* plan);
 const char* sas_last_error(void);
 const char* sas_version(void);

@@ -30,6 +30,7 @@ EXPORTS = (
     "sas_plan_create", "sas_solve", "sas_solve_host", "sas_lift", "sas_residual",
     "sas_plan_set_operator", "sas_plan_info", "sas_last_launch_count",
     "sas_plan_destroy", "sas_last_error", "sas_version", "sas_plan_set_timing", "sas_stage_times",
+    "sas_tsqr_r",
 )
 SAS_STAGE_LSQ, SAS_STAGE_GAUSS_ROWS = 1, 2
 #: test-only symbols (include/sas_debug.h)
@@ -95,6 +96,8 @@ def _declare(lib):
     lib.sas_debug_exp64_host.restype = C.c_double
     lib.sas_debug_exp64.argtypes = [vp, vp, i64, vp]
     lib.sas_debug_exp64.restype = C.c_int
+    lib.sas_tsqr_r.argtypes = [vp, i64, i32, i32, vp, i32, vp]
+    lib.sas_tsqr_r.restype = C.c_int
     return lib
 
 

@@ -20,6 +20,7 @@
 #include "k_lsq_mw.cuh"
 #include "k_lsq_cw.cuh"
 #include "k_lsq_sm.cuh"
+#include "k_tsqr.cuh"
 #include "k_gauss.cuh"
 #include "k_recon.cuh"
 
@@ -1245,4 +1246,49 @@ extern "C" int sas_residual(sas_plan* pl, const void* params, const void* coef, 
   pl->last_launches++;
   SAS_CUDA_CHECK(cudaGetLastError());
   return SAS_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// TSQR (k_tsqr.cuh): R of an m x w row-major device matrix, level by level.
+template <typename T, int RA, int W>
+static int tsqr_t(const T* A, int64_t m, int w, T* R, cudaStream_t st) {
+  constexpr int MB = 32 * RA;
+  const size_t smem = tsqr_smem_bytes(RA, w, sizeof(T));
+  SMEM_OPTIN(k_tsqr_block<T, RA, W>);
+  int64_t nb0 = (m + MB - 1) / MB;
+  T* buf[2] = {nullptr, nullptr};
+  if (nb0 > 1) {
+    const int64_t nb1 = (nb0 * w + MB - 1) / MB;
+    SAS_CUDA_CHECK(cudaMallocAsync((void**)&buf[0], (size_t)nb0 * w * w * sizeof(T), st));
+    SAS_CUDA_CHECK(cudaMallocAsync((void**)&buf[1], (size_t)(nb1 > 1 ? nb1 : 1) * w * w * sizeof(T), st));
+  }
+  const T* cur = A;
+  int64_t rows = m;
+  for (int lvl = 0;; ++lvl) {
+    const int64_t nb = (rows + MB - 1) / MB;
+    T* dst = (nb == 1) ? R : buf[lvl & 1];
+    k_tsqr_block<T, RA, W><<<(unsigned)nb, 32 * W, smem, st>>>(cur, rows, w, dst);
+    SAS_CUDA_CHECK(cudaGetLastError());
+    if (nb == 1) break;
+    cur = dst;
+    rows = nb * w;
+  }
+  if (buf[0]) SAS_CUDA_CHECK(cudaFreeAsync(buf[0], st));
+  if (buf[1]) SAS_CUDA_CHECK(cudaFreeAsync(buf[1], st));
+  return SAS_OK;
+}
+
+extern "C" int sas_tsqr_r(const void* A, int64_t m, int32_t w, int32_t dtype, void* R, int32_t device,
+                          void* stream) {
+  ARG_CHECK(A && R, "sas_tsqr_r: null pointer");
+  ARG_CHECK(m >= 1 && w >= 1 && w <= 64, "sas_tsqr_r: need m >= 1 and 1 <= w <= 64 (m=%lld w=%d)", (long long)m, w);
+  ARG_CHECK(dtype == SAS_F64 || dtype == SAS_C128, "sas_tsqr_r: dtype must be SAS_F64 or SAS_C128");
+  DevGuard g(device);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == SAS_F64) {
+    if (w <= 48) return tsqr_t<double, 8, 16>((const double*)A, m, w, (double*)R, st);
+    return tsqr_t<double, 4, 16>((const double*)A, m, w, (double*)R, st);
+  }
+  return tsqr_t<cplx, 4, 16>((const cplx*)A, m, w, (cplx*)R, st);
 }

@@ -558,12 +558,32 @@ def _operator_times_basis(system, X, p, dev):
     raise ValueError("system has no GPU operator")
 
 
+def tsqr_r(A, device: int = 0):
+    """R factor (w x w, upper triangular) of a tall m x w CUDA tensor (w <= 64,
+    float64 or complex128) by the TSQR kernel tree of libsas (k_tsqr_block,
+    sas_tsqr_r): block Householder QRs in shared memory, then the stacked R
+    blocks, level by level.  R equals numpy's qr R up to the signs of its rows."""
+    import torch
+    A = A.contiguous()
+    m, w = A.shape
+    R = torch.empty((w, w), dtype=A.dtype, device=A.device)
+    lib = _capi.load()
+    st = torch.cuda.current_stream(A.device)
+    dt = _capi.SAS_C128 if A.is_complex() else _capi.SAS_F64
+    _capi.check(lib.sas_tsqr_r(_capi.ptr(A), m, w, dt, _capi.ptr(R), int(A.device.index or 0),
+                               C.c_void_p(st.cuda_stream)), "sas_tsqr_r")
+    return R
+
+
 def solve_apsnap(system, basis, p, device: int = 0):
     """Full least squares min ||A(p) Q_X c - b(p)|| (online.py:156-165) on the
-    GPU: B = A(p) X from the GPU operator, Householder QR (cuSOLVER via
-    torch.linalg.qr), the reference's 1e-12 rank test (linalg.py:107-112) and a
-    triangular solve.  Returns (coefficients, true residual norm).  Not on the
+    GPU: B = A(p) X from the GPU operator, the R factor of [B | b] by libsas's
+    TSQR kernels (sas_tsqr_r), the reference's 1e-12 rank test on |R_ii|
+    (linalg.py:107-112), c from the triangular system R c = (Q^H b)[:r'] (the
+    last column of R), and the true residual ||B c - b|| recomputed explicitly
+    as the reference does.  Returns (coefficients, residual).  Not on the
     online hot path: O(n r'^2) per parameter."""
+    import scipy.linalg as sla
     import torch
     dev = torch.device(f"cuda:{device}")
     X = torch.from_numpy(np.ascontiguousarray(basis.basis)).to(dev)
@@ -574,14 +594,17 @@ def solve_apsnap(system, basis, p, device: int = 0):
     rhs = rhs.to(B.dtype)
     if not bool(torch.isfinite(B).all()):
         raise ValueError("matrix has non-finite entries")   # linalg._as_matrix, linalg.py:36-37
-    q, rmat = torch.linalg.qr(B, mode="reduced")
-    diag = rmat.diagonal().abs()
-    if diag.numel() and float(diag.min()) < 1e-12 * max(float(diag.max()), np.finfo(float).tiny):
-        raise RankDeficiencyError(f"rank-deficient least-squares matrix at column {int(diag.argmin())}")
-    y = q.conj().transpose(0, 1) @ rhs
-    coeff = torch.linalg.solve_triangular(rmat, y[:, None], upper=True)[:, 0]
-    residual = float(torch.linalg.norm(B @ coeff - rhs))
-    return coeff.cpu().numpy(), residual
+    n, r = B.shape
+    if n < r:
+        raise ValueError("solve_ls requires rows >= cols")
+    R = tsqr_r(torch.cat([B, rhs[:, None]], dim=1), device=device).cpu().numpy()
+    diag = np.abs(np.diag(R)[:r])
+    if diag.size and diag.min() < 1e-12 * max(diag.max(), np.finfo(float).tiny):
+        raise RankDeficiencyError(f"rank-deficient least-squares matrix at column {int(np.argmin(diag))}")
+    coeff = sla.solve_triangular(R[:r, :r], R[:r, r])
+    c_t = torch.from_numpy(np.ascontiguousarray(coeff)).to(dev)
+    residual = float(torch.linalg.norm(B @ c_t - rhs))
+    return coeff, residual
 
 
 # --------------------------------------------------------------------------
