@@ -186,6 +186,19 @@ int32_t sas_stage_times(sas_plan* plan, float* ms, int32_t* stage, int32_t cap);
  * Stream-ordered; scratch comes from the stream-ordered allocator. */
 int sas_tsqr_r(const void* A, int64_t m, int32_t w, int32_t dtype, void* R, int32_t device, void* stream);
 
+/* Offline snapshot solve of a stencil system (replaces full_solve,
+ * systems.py:187-222, for configs 3 and 5): Jacobi-preconditioned CG on
+ *   (A v)_i = dg_i v_i - sum_e ct[i][e] v_{nbr[i][e]}   (nbr = -1: Dirichlet edge)
+ * with fused kernels (q = A p with the direction update, then the vector
+ * updates with their dot products).  Stops at ||r|| <= tol ||b|| or
+ * ||r|| <= 1e-12 (a_norm ||x|| + ||b||), checked every check_every iterations.
+ * All arrays device (n, n x E); outputs: iterations, the TRUE residual
+ * ||b - A x|| and ||x|| (the caller applies the reference's residual guard). */
+int sas_cg_stencil(int64_t n, int32_t E, const double* dg, const double* ct, const int64_t* nbr,
+                   const double* b, double* x, double tol, double a_norm, int32_t maxiter,
+                   int32_t check_every, int32_t device, void* stream, int32_t* iters_out,
+                   double* rnorm_out, double* xnorm_out);
+
 void sas_plan_destroy(sas_plan* plan);
 const char* sas_last_error(void);
 const char* sas_version(void);

@@ -21,6 +21,7 @@
 #include "k_lsq_cw.cuh"
 #include "k_lsq_sm.cuh"
 #include "k_tsqr.cuh"
+#include "k_cg.cuh"
 #include "k_gauss.cuh"
 #include "k_recon.cuh"
 
@@ -1291,4 +1292,83 @@ extern "C" int sas_tsqr_r(const void* A, int64_t m, int32_t w, int32_t dtype, vo
     return tsqr_t<double, 4, 16>((const double*)A, m, w, (double*)R, st);
   }
   return tsqr_t<cplx, 4, 16>((const cplx*)A, m, w, (cplx*)R, st);
+}
+
+
+// ---------------------------------------------------------------------------
+// Jacobi-preconditioned CG for the stencil snapshot solves (k_cg.cuh).
+extern "C" int sas_cg_stencil(int64_t n, int32_t E, const double* dg, const double* ct, const int64_t* nbr,
+                              const double* b, double* x, double tol, double a_norm, int32_t maxiter,
+                              int32_t check_every, int32_t device, void* stream, int32_t* iters_out,
+                              double* rnorm_out, double* xnorm_out) {
+  ARG_CHECK(n >= 1 && E >= 1 && E <= 8, "sas_cg_stencil: need n >= 1 and 1 <= E <= 8");
+  ARG_CHECK(dg && ct && nbr && b && x, "sas_cg_stencil: null device pointer");
+  ARG_CHECK(maxiter >= 1 && check_every >= 1, "sas_cg_stencil: maxiter and check_every must be >= 1");
+  DevGuard g(device);
+  cudaStream_t st = (cudaStream_t)stream;
+  int sms = 0;
+  SAS_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  int nb = (int)std::min<int64_t>((n + kCgThreads - 1) / kCgThreads, (int64_t)sms * 8);
+  double *r = nullptr, *z = nullptr, *pb = nullptr, *q = nullptr, *part = nullptr, *ppq = nullptr;
+  SAS_CUDA_CHECK(cudaMallocAsync((void**)&r, n * sizeof(double), st));
+  SAS_CUDA_CHECK(cudaMallocAsync((void**)&z, n * sizeof(double), st));
+  SAS_CUDA_CHECK(cudaMallocAsync((void**)&pb, 2 * n * sizeof(double), st));
+  SAS_CUDA_CHECK(cudaMallocAsync((void**)&q, n * sizeof(double), st));
+  SAS_CUDA_CHECK(cudaMallocAsync((void**)&part, 3 * 2 * (size_t)nb * sizeof(double), st));
+  SAS_CUDA_CHECK(cudaMallocAsync((void**)&ppq, (size_t)nb * sizeof(double), st));
+  std::vector<double> hp(2 * (size_t)nb);
+  auto host_sum = [&](const double* dpart, int comp, double* out) -> int {
+    SAS_CUDA_CHECK(cudaMemcpyAsync(hp.data(), dpart, 2 * (size_t)nb * sizeof(double), cudaMemcpyDeviceToHost, st));
+    SAS_CUDA_CHECK(cudaStreamSynchronize(st));
+    double t = 0.0;
+    for (int i = 0; i < nb; ++i) t += hp[2 * (size_t)i + comp];
+    *out = t;
+    return SAS_OK;
+  };
+  int rc = SAS_OK;
+  double bn2 = 0.0, rn = 0.0, xn = 0.0;
+  int it = 0;
+  k_cg_init<<<nb, kCgThreads, 0, st>>>(n, dg, b, x, r, z, part);
+  if ((rc = host_sum(part, 1, &bn2))) return rc;
+  const double bn = sqrt(bn2);
+  rn = bn;
+  for (it = 0; it < maxiter; ++it) {
+    double* pnew = pb + (size_t)(it & 1) * n;
+    const double* pold = pb + (size_t)((it + 1) & 1) * n;
+    const double* prz = part + 2 * (size_t)nb * (it % 3);
+    const double* prz0 = part + 2 * (size_t)nb * ((it + 2) % 3);
+    double* pout = part + 2 * (size_t)nb * ((it + 1) % 3);
+    k_cg_apply<<<nb, kCgThreads, 0, st>>>(n, E, dg, ct, nbr, z, pold, pnew, q, prz, prz0, it == 0 ? 1 : 0, ppq);
+    k_cg_update<<<nb, kCgThreads, 0, st>>>(n, dg, pnew, q, x, r, z, prz, ppq, pout);
+    if ((it + 1) % check_every == 0 || it + 1 == maxiter) {
+      double rr = 0.0;
+      if ((rc = host_sum(pout, 1, &rr))) return rc;
+      rn = sqrt(rr);
+      if (!(rn == rn)) break;  // NaN: breakdown
+      if (rn <= tol * bn) { ++it; break; }
+      k_cg_true_resid<<<nb, kCgThreads, 0, st>>>(n, E, dg, ct, nbr, x, b, part + 2 * (size_t)nb * ((it + 2) % 3));
+      // (that buffer holds rz_{it-1}, which the next iteration no longer reads)
+      double xx = 0.0;
+      if ((rc = host_sum(part + 2 * (size_t)nb * ((it + 2) % 3), 1, &xx))) return rc;
+      if (rn <= 1e-12 * (a_norm * sqrt(xx) + bn)) { ++it; break; }
+    }
+  }
+  SAS_CUDA_CHECK(cudaGetLastError());
+  // final true residual and |x|
+  k_cg_true_resid<<<nb, kCgThreads, 0, st>>>(n, E, dg, ct, nbr, x, b, part);
+  double rr = 0.0, xx = 0.0;
+  if ((rc = host_sum(part, 0, &rr))) return rc;
+  if ((rc = host_sum(part, 1, &xx))) return rc;
+  xn = sqrt(xx);
+  if (iters_out) *iters_out = it;
+  if (rnorm_out) *rnorm_out = sqrt(rr);
+  if (xnorm_out) *xnorm_out = xn;
+  cudaFreeAsync(r, st);
+  cudaFreeAsync(z, st);
+  cudaFreeAsync(pb, st);
+  cudaFreeAsync(q, st);
+  cudaFreeAsync(part, st);
+  cudaFreeAsync(ppq, st);
+  SAS_CUDA_CHECK(cudaStreamSynchronize(st));
+  return SAS_OK;
 }

@@ -152,65 +152,54 @@ def _gauss_solve_all(op: GaussianKernelOperator, b: np.ndarray, points, device=N
 
 
 def _stencil_tensors(system, device):
-    """All nodes' neighbours and edge-midpoint basis values on the device (once per system)."""
+    """All nodes' neighbours (-1 on Dirichlet edges) and edge-midpoint basis
+    values on the device (once per system)."""
     import torch
     op: StencilOperator = system.operator
     nbr, phi = op.edges(np.arange(op.n))
-    inside = torch.from_numpy(nbr >= 0).to(device)
-    return {"nt": torch.from_numpy(np.where(nbr >= 0, nbr, 0)).to(device), "inside": inside,
-            "phi": torch.from_numpy(phi).to(device),
+    return {"nbr": torch.from_numpy(nbr).to(device), "phi": torch.from_numpy(phi).to(device),
             "b": torch.from_numpy(np.asarray(system.b, dtype=float)).to(device)}
 
 
 def _stencil_cg(system, p, device, tol=1e-11, maxiter=50_000, tensors=None):
-    """Jacobi-preconditioned CG on the GPU for the SPD stencil operator.
-    Stops at ||r|| <= tol ||b|| or, if that is below what fp64 CG can attain
-    for this conditioning, once the reference's full_solve guard
-    ||r|| <= 1e-10 (||A|| ||x|| + ||b||) holds with a 100x margin
-    (systems.py:205-221)."""
+    """Jacobi-preconditioned CG on the GPU for the SPD stencil operator, by
+    libsas's fused CG kernels (k_cg.cuh, sas_cg_stencil: q = A p with the
+    search-direction update fused in, then x/r/z updates with the dot
+    products; no host round trip between iterations).  Stops at
+    ||r|| <= tol ||b|| or, if that is below what fp64 CG can attain for this
+    conditioning, once ||r|| <= 1e-12 (||A|| ||x|| + ||b||); the reference's
+    full_solve guard ||r|| <= 1e-10 (||A|| ||x|| + ||b||) is then checked on
+    the true residual (systems.py:205-221)."""
+    import ctypes as C
+
     import torch
+
+    from . import _capi
     op: StencilOperator = system.operator
     tz = tensors if tensors is not None else _stencil_tensors(system, device)
     pv = np.asarray(p, dtype=float).ravel()
-    phi = tz["phi"]
+    phi, nbr, b = tz["phi"], tz["nbr"], tz["b"]
     arg = phi[..., 0] * float(pv[0])
     for k in range(1, pv.size):
         arg = arg + phi[..., k] * float(pv[k])
     c = torch.exp(arg) / (op.h * op.h)
-    dg = c.sum(dim=1)
-    ct = torch.where(tz["inside"], c, torch.zeros_like(c))
-    nt = tz["nt"]
-    b = tz["b"]
-    del c, arg
-
-    def A(v):
-        return dg * v - (ct * v[nt]).sum(dim=1)
-
-    x = torch.zeros_like(b)
-    r = b.clone()
-    z = r / dg
-    pdir = z.clone()
-    rz = torch.dot(r, z)
-    bn = torch.linalg.norm(b)
+    del arg
+    dg = c.sum(dim=1).contiguous()
+    ct = torch.where(nbr >= 0, c, torch.zeros_like(c)).contiguous()
+    del c
+    bn = float(torch.linalg.norm(b))
     a_norm = float(torch.sqrt((dg * dg).sum() + (ct * ct).sum()))
-    for it in range(maxiter):
-        Ap = A(pdir)
-        alpha = rz / torch.dot(pdir, Ap)
-        x += alpha * pdir
-        r -= alpha * Ap
-        if it % 50 == 0:
-            rn = float(torch.linalg.norm(r))
-            if rn <= tol * float(bn) or rn <= 1e-12 * (a_norm * float(torch.linalg.norm(x)) + float(bn)):
-                break
-        z = r / dg
-        rz_new = torch.dot(r, z)
-        pdir = z + (rz_new / rz) * pdir
-        rz = rz_new
-    r = b - A(x)  # true residual
-    res = float(torch.linalg.norm(r))
-    floor = a_norm * float(torch.linalg.norm(x)) + float(bn)
-    if res > FULL_SOLVE_RTOL * floor:
-        raise NumericalError(f"CG snapshot solve failed at p={p}: residual {res:.3e}")
+    x = torch.empty_like(b)
+    its, rn, xn = C.c_int32(0), C.c_double(0.0), C.c_double(0.0)
+    lib = _capi.load()
+    dev_index = b.device.index or 0
+    st = torch.cuda.current_stream(b.device)
+    _capi.check(lib.sas_cg_stencil(op.n, op.n_edges, _capi.ptr(dg), _capi.ptr(ct), _capi.ptr(nbr), _capi.ptr(b),
+                                   _capi.ptr(x), tol, a_norm, maxiter, 50, dev_index, C.c_void_p(st.cuda_stream),
+                                   C.byref(its), C.byref(rn), C.byref(xn)), "sas_cg_stencil")
+    if not math.isfinite(rn.value) or rn.value > FULL_SOLVE_RTOL * (a_norm * xn.value + bn):
+        raise NumericalError(f"CG snapshot solve failed at p={p}: residual {rn.value:.3e} after {its.value} "
+                             f"iterations")
     return x.cpu().numpy()
 
 
