@@ -144,11 +144,23 @@ int sas_solve_host(sas_plan* plan, const void* params, int64_t P,
  * device (kept by every plan). */
 int sas_lift(sas_plan* plan, const void* coef, int64_t P, void* x, void* stream);
 
-/* Full relative residual ||A(p) x - b|| / max(||b||, 1e-300) of x = X c
- * (cli.py:344-351) without materialising x; needs the full operator
- * (sas_plan_set_operator).  params/coef device, relres out P doubles device. */
+/* Full relative residual ||A(p) x - b(p)|| / max(||b(p)||, 1e-300) of x = X c
+ * (cli.py:344-351); needs the full operator (sas_plan_set_operator).
+ *   params      P x d_p (x2 if param_complex), device
+ *   coef        P x r (dtype), device
+ *   coef_table  P x K x 2 doubles (SAS_COEF_TABLE terms) or NULL, device
+ *   b_table     P x n (dtype) right-hand sides b(p), or NULL for the plan's
+ *               constant b (stencil plans: NULL only), device
+ *   relres      out, P doubles, device
+ *   floor_est   out, P doubles or NULL: the rounding floor
+ *               100 eps || |A(p)| |x| || / ||b(p)|| below
+ *               which a relative residual is noise, device
+ * Stencil plans never materialise A(p) (edge coefficients re-evaluated per
+ * parameter); affine plans run the K CSR terms; Gaussian plans re-evaluate
+ * kernel rows (n^2 exps per parameter: meant for small subsets). */
 int sas_residual(sas_plan* plan, const void* params, const void* coef, int64_t P,
-                 double* relres, void* stream);
+                 const double* coef_table, const void* b_table, double* relres,
+                 double* floor_est, void* stream);
 
 /* Full operator for sas_residual (CSR per affine term, or the full stencil
  * description, or nothing for SAS_OP_GAUSS which re-evaluates kernel rows).

@@ -73,7 +73,7 @@ def _declare(lib):
     lib.sas_solve_host.restype = C.c_int
     lib.sas_lift.argtypes = [vp, vp, i64, vp, vp]
     lib.sas_lift.restype = C.c_int
-    lib.sas_residual.argtypes = [vp, vp, vp, i64, vp, vp]
+    lib.sas_residual.argtypes = [vp, vp, vp, i64, vp, vp, vp, vp, vp]
     lib.sas_residual.restype = C.c_int
     lib.sas_plan_set_operator.argtypes = [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), vp, vp, vp]
     lib.sas_plan_set_operator.restype = C.c_int

@@ -119,14 +119,17 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return t;  // valid on thread 0
 }
 
-// Affine residual: sum_k f_k(p) A_k x - b with CSR A_k, for one p per blockIdx.y.
+// Affine residual: sum_k f_k(p) A_k x - b(p) with CSR A_k, for one p per
+// blockIdx.y (b(p) = b + p * b_stride: b_stride = 0 for a constant rhs, n for
+// a P x n table).  Per-CTA partials (|r|^2, |b|^2, || |A| |x| ||^2), the last
+// for the rounding floor 100 eps || |A| |x| || / ||b||.
 template <typename T>
 __global__ void __launch_bounds__(256) k_resid_affine(const T* __restrict__ X, int64_t n, int r, int K,
                                                       const int64_t* const* __restrict__ rp,
                                                       const int64_t* const* __restrict__ ci,
                                                       const T* const* __restrict__ va,
                                                       const T* __restrict__ fcoef,  // P x K
-                                                      const T* __restrict__ b,
+                                                      const T* __restrict__ b, int64_t b_stride,
                                                       const T* __restrict__ coef,   // P x r
                                                       double* __restrict__ part) {
   using S = Sc<T>;
@@ -135,37 +138,48 @@ __global__ void __launch_bounds__(256) k_resid_affine(const T* __restrict__ X, i
   const int64_t p = blockIdx.y;
   for (int j = threadIdx.x; j < r; j += blockDim.x) cs[j] = coef[p * r + j];
   __syncthreads();
-  double rr = 0.0, bb = 0.0;
+  const T* bp = b + p * b_stride;
+  double rr = 0.0, bb = 0.0, aa = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     T ax = S::zero();
+    double absax = 0.0;
     for (int k = 0; k < K; ++k) {
       T rowacc = S::zero();
+      double absrow = 0.0;
       for (int64_t q = rp[k][i]; q < rp[k][i + 1]; ++q) {
         const int64_t m = ci[k][q];
         T xm = S::zero();
         for (int j = 0; j < r; ++j) xm = S::add(xm, S::mul(X[m * r + j], cs[j]));
         rowacc = S::add(rowacc, S::mul(va[k][q], xm));
+        absrow += S::abs(va[k][q]) * S::abs(xm);
       }
-      ax = S::add(ax, S::mul(fcoef[p * K + k], rowacc));
+      const T f = fcoef[p * K + k];
+      ax = S::add(ax, S::mul(f, rowacc));
+      absax += S::abs(f) * absrow;
     }
-    const T res = S::sub(ax, b[i]);
+    const T res = S::sub(ax, bp[i]);
     rr += S::abs2(res);
-    bb += S::abs2(b[i]);
+    bb += S::abs2(bp[i]);
+    aa = fma(absax, absax, aa);
   }
   double trr = block_sum(rr, red);
   double tbb = block_sum(bb, red);
+  double taa = block_sum(aa, red);
   if (threadIdx.x == 0) {
-    part[(p * gridDim.x + blockIdx.x) * 2] = trr;
-    part[(p * gridDim.x + blockIdx.x) * 2 + 1] = tbb;
+    double* o = part + (p * gridDim.x + blockIdx.x) * 3;
+    o[0] = trr;
+    o[1] = tbb;
+    o[2] = taa;
   }
 }
 
-// Gaussian-kernel residual: (K_p + ridge I) x - b with kernel entries
+// Gaussian-kernel residual: (K_p + ridge I) x - b(p) with kernel entries
 // re-evaluated on the fly (n^2 exps per p; used on a small subset of p).
+// Partials as k_resid_affine (K_p >= 0: |A| |x| = K_p |x| + |lam| |x_i|).
 __global__ void __launch_bounds__(256) k_resid_gauss(const double* __restrict__ X, int64_t n, int r,
                                                      const double* __restrict__ pts, int d,
                                                      double ridge, int dp, const double* __restrict__ b,
-                                                     const double* __restrict__ params,
+                                                     int64_t b_stride, const double* __restrict__ params,
                                                      const double* __restrict__ xfull,  // P x n (lifted)
                                                      double* __restrict__ part) {
   __shared__ double red[32];
@@ -174,10 +188,11 @@ __global__ void __launch_bounds__(256) k_resid_gauss(const double* __restrict__ 
   const double lam = (dp == 2) ? params[p * 2] : ridge;
   const double inv = 1.0 / (2.0 * sg * sg);
   const double* x = xfull + p * n;
-  double rr = 0.0, bb = 0.0;
+  const double* bp = b + p * b_stride;
+  double rr = 0.0, bb = 0.0, aa = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double* xi = pts + i * d;
-    double acc = 0.0;
+    double acc = 0.0, absacc = 0.0;
     for (int64_t l = 0; l < n; ++l) {
       const double* xl = pts + l * d;
       double dd = 0.0;
@@ -188,29 +203,40 @@ __global__ void __launch_bounds__(256) k_resid_gauss(const double* __restrict__ 
       double kv = exp(-(dd * inv));
       if (l == i) kv += lam;
       acc = fma(kv, x[l], acc);
+      absacc = fma(fabs(kv), fabs(x[l]), absacc);
     }
-    const double res = acc - b[i];
+    const double res = acc - bp[i];
     rr = fma(res, res, rr);
-    bb = fma(b[i], b[i], bb);
+    bb = fma(bp[i], bp[i], bb);
+    aa = fma(absacc, absacc, aa);
   }
   double trr = block_sum(rr, red);
   double tbb = block_sum(bb, red);
+  double taa = block_sum(aa, red);
   if (threadIdx.x == 0) {
-    part[(p * gridDim.x + blockIdx.x) * 2] = trr;
-    part[(p * gridDim.x + blockIdx.x) * 2 + 1] = tbb;
+    double* o = part + (p * gridDim.x + blockIdx.x) * 3;
+    o[0] = trr;
+    o[1] = tbb;
+    o[2] = taa;
   }
 }
 
-// relres[p] = sqrt(sum rr) / max(sqrt(sum bb), 1e-300), fixed-order sum over CTAs.
-__global__ void k_resid_finish(const double* __restrict__ part, int nb, int64_t P, double* __restrict__ relres) {
+// relres[p] = sqrt(sum rr) / max(sqrt(sum bb), 1e-300) and the rounding floor
+// floor[p] = 100 eps sqrt(sum aa) / max(sqrt(sum bb), 1e-300) (nullable),
+// fixed-order sums over the CTAs' (rr, bb, aa) partials.
+__global__ void k_resid_finish(const double* __restrict__ part, int nb, int64_t P, double* __restrict__ relres,
+                               double* __restrict__ floor_est) {
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (p >= P) return;
-  double rr = 0.0, bb = 0.0;
+  double rr = 0.0, bb = 0.0, aa = 0.0;
   for (int q = 0; q < nb; ++q) {
-    rr += part[(p * nb + q) * 2];
-    bb += part[(p * nb + q) * 2 + 1];
+    rr += part[(p * nb + q) * 3];
+    bb += part[(p * nb + q) * 3 + 1];
+    aa += part[(p * nb + q) * 3 + 2];
   }
-  relres[p] = sqrt(rr) / fmax(sqrt(bb), 1e-300);
+  const double bn = fmax(sqrt(bb), 1e-300);
+  relres[p] = sqrt(rr) / bn;
+  if (floor_est) floor_est[p] = 100.0 * 2.220446049250313e-16 * sqrt(aa) / bn;
 }
 
 constexpr int kResidPB = 16;   // parameter values per pass: one 128-byte line of x per node
@@ -227,7 +253,7 @@ constexpr int kResidPT = kResidPB / kResidTPN;
 // table exp.  Eight consecutive lanes share a node (2 parameter values each):
 // x_i and x_m are whole aligned 128-byte lines read by 8 lanes, the node's phi
 // and neighbour indices are broadcast loads serving 16 parameter values.
-// grid = (nb, passes); partial sums of |r|^2 and |b|^2 per CTA and parameter.
+// grid = (nb, passes); partial sums of |r|^2, |b|^2 and || |A| |x| ||^2 per CTA and parameter.
 __global__ void __launch_bounds__(256, 2) k_resid_stencil_b16(const double* __restrict__ x, int64_t n, int64_t P,
                                                            const int64_t* __restrict__ nbr,
                                                            const double* __restrict__ phi, int E, int dp, double hh,
@@ -238,6 +264,7 @@ __global__ void __launch_bounds__(256, 2) k_resid_stencil_b16(const double* __re
   __shared__ double ps[kResidPB * 8];
   __shared__ double tab_s[2048];
   __shared__ double rsum[kResidPB][8];
+  __shared__ double asum[kResidPB][8];
   for (int j = threadIdx.x; j < 2048; j += blockDim.x) tab_s[j] = g_exp2_tab2048[j];
   const double inv_hh = 1.0 / hh;
   const int64_t pb = (int64_t)blockIdx.y * kResidPB;
@@ -255,13 +282,13 @@ __global__ void __launch_bounds__(256, 2) k_resid_stencil_b16(const double* __re
   for (int u = 0; u < kResidPT; ++u)
 #pragma unroll
     for (int k = 0; k < 8; ++k) pu[u][k] = ps[(u0 + u) * 8 + k];
-  double rr[kResidPT];
+  double rr[kResidPT], aa[kResidPT];
 #pragma unroll
-  for (int u = 0; u < kResidPT; ++u) rr[u] = 0.0;
+  for (int u = 0; u < kResidPT; ++u) rr[u] = aa[u] = 0.0;
   double bb = 0.0;
   const int64_t nstride = (int64_t)gridDim.x * blockDim.x / kResidTPN;
   for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kResidTPN; i < n; i += nstride) {
-    double xi[kResidPT], acc[kResidPT];
+    double xi[kResidPT], acc[kResidPT], absacc[kResidPT];
 #pragma unroll
     for (int h = 0; h < kResidPT / 2; ++h) {
       const double2 v = __ldg(xb + i * (kResidPB / 2) + h);
@@ -269,7 +296,7 @@ __global__ void __launch_bounds__(256, 2) k_resid_stencil_b16(const double* __re
       xi[2 * h + 1] = v.y;
     }
 #pragma unroll
-    for (int u = 0; u < kResidPT; ++u) acc[u] = 0.0;
+    for (int u = 0; u < kResidPT; ++u) acc[u] = absacc[u] = 0.0;
     for (int e = 0; e < E; ++e) {
       const double* ph = phi + (i * E + e) * dp;
       double phv[8];
@@ -291,6 +318,7 @@ __global__ void __launch_bounds__(256, 2) k_resid_stencil_b16(const double* __re
           if (k < dp) arg = fma(pu[u][k], phv[k], arg);
         const double c = sas_exp64_t2k(arg, tab_s) * inv_hh;
         acc[u] = fma(c, xi[u] - xm[u], acc[u]);
+        absacc[u] = fma(c, fabs(xi[u]) + fabs(xm[u]), absacc[u]);   // |A| |x|: c_e > 0
       }
     }
     const double bi = __ldg(b + i);
@@ -298,6 +326,7 @@ __global__ void __launch_bounds__(256, 2) k_resid_stencil_b16(const double* __re
     for (int u = 0; u < kResidPT; ++u) {
       const double res = acc[u] - bi;
       rr[u] = fma(res, res, rr[u]);
+      aa[u] = fma(absacc[u], absacc[u], aa[u]);
     }
     if (sub == 0) bb = fma(bi, bi, bb);
   }
@@ -305,17 +334,27 @@ __global__ void __launch_bounds__(256, 2) k_resid_stencil_b16(const double* __re
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
   for (int u = 0; u < kResidPT; ++u) {
-    double v = rr[u];
+    double v = rr[u], w2 = aa[u];
 #pragma unroll
-    for (int off = kResidTPN; off < 32; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    if (lane < kResidTPN) rsum[u0 + u][warp] = v;
+    for (int off = kResidTPN; off < 32; off <<= 1) {
+      v += __shfl_xor_sync(0xffffffffu, v, off);
+      w2 += __shfl_xor_sync(0xffffffffu, w2, off);
+    }
+    if (lane < kResidTPN) {
+      rsum[u0 + u][warp] = v;
+      asum[u0 + u][warp] = w2;
+    }
   }
   const double tbb = block_sum(bb, red);  // (its __syncthreads also publishes rsum)
   if (threadIdx.x < npb) {
-    double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += rsum[threadIdx.x][w];
-    part[((pb + threadIdx.x) * gridDim.x + blockIdx.x) * 2] = t;
+    double t = 0.0, ta = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      t += rsum[threadIdx.x][w];
+      ta += asum[threadIdx.x][w];
+    }
+    part[((pb + threadIdx.x) * gridDim.x + blockIdx.x) * 3] = t;
+    part[((pb + threadIdx.x) * gridDim.x + blockIdx.x) * 3 + 2] = ta;
   }
   if (threadIdx.x == 0)
-    for (int u = 0; u < npb; ++u) part[((pb + u) * gridDim.x + blockIdx.x) * 2 + 1] = tbb;
+    for (int u = 0; u < npb; ++u) part[((pb + u) * gridDim.x + blockIdx.x) * 3 + 1] = tbb;
 }

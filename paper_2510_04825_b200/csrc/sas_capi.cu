@@ -1177,7 +1177,8 @@ __global__ void k_affine_coefs(const int32_t* kind, const double* scale, const d
   f[idx] = AffineCoef<T>::eval(kind[k], sc, rt, pv.get(p, 0), ctab ? ctab + idx * 2 : nullptr);
 }
 
-extern "C" int sas_residual(sas_plan* pl, const void* params, const void* coef, int64_t P, double* relres,
+extern "C" int sas_residual(sas_plan* pl, const void* params, const void* coef, int64_t P,
+                            const double* coef_table, const void* b_table, double* relres, double* floor_est,
                             void* stream) {
   ARG_CHECK(pl, "null plan");
   if (P == 0) return SAS_OK;
@@ -1190,13 +1191,16 @@ extern "C" int sas_residual(sas_plan* pl, const void* params, const void* coef, 
   int nb = (int)((pl->n + 255) / 256);
   if (nb > pl->sms * 4) nb = pl->sms * 4;
   int rc;
-  if ((rc = ensure(&pl->rpart, &pl->rpart_n, P * nb * 2 * (int64_t)sizeof(double)))) return rc;
+  if ((rc = ensure(&pl->rpart, &pl->rpart_n, P * nb * 3 * (int64_t)sizeof(double)))) return rc;
   pl->last_launches = 0;
   dim3 grid(nb, (unsigned)P);
+  const void* bvec = b_table ? b_table : pl->full_b;
+  const int64_t bstride = b_table ? pl->n : 0;
   if (pl->op == SAS_OP_STENCIL) {
     // x for a chunk of (up to) 64 parameters (K5, DMMA, one X pass per chunk),
     // stored in 16-parameter blocks, then the stencil residual on it (K6)
     ARG_CHECK(pl->full_nbr, "sas_residual: stencil operator not set");
+    ARG_CHECK(!b_table, "sas_residual: stencil systems take the plan's constant right-hand side");
     const int64_t chunk = P < 64 ? ((P + kResidPB - 1) / kResidPB) * kResidPB : 64;
     if ((rc = ensure(&pl->xscr, &pl->xscr_n, chunk * pl->n * (int64_t)sizeof(double)))) return rc;
     for (int64_t p0 = 0; p0 < P; p0 += chunk) {
@@ -1205,29 +1209,30 @@ extern "C" int sas_residual(sas_plan* pl, const void* params, const void* coef, 
       dim3 g2(nb, (unsigned)((pc + kResidPB - 1) / kResidPB));
       k_resid_stencil_b16<<<g2, 256, 0, st>>>(pl->xscr, pl->n, pc, pl->full_nbr, pl->full_phi, pl->E, pl->dp, pl->hh,
                                               (const double*)pl->full_b, (const double*)params + p0 * pl->dp,
-                                              pl->rpart + p0 * nb * 2);
+                                              pl->rpart + p0 * nb * 3);
       pl->last_launches += 2;
     }
   } else if (pl->op == SAS_OP_AFFINE) {
     ARG_CHECK(!pl->csr_rp.empty(), "sas_residual: affine operator not set");
     for (int k = 0; k < pl->K; ++k)
-      ARG_CHECK(pl->h_kind[k] != SAS_COEF_TABLE, "sas_residual: table coefficients not supported");
+      ARG_CHECK(pl->h_kind[k] != SAS_COEF_TABLE || coef_table,
+                "sas_residual: coefficient table required for SAS_COEF_TABLE terms");
     if ((rc = ensure(&pl->fco, &pl->fco_n, P * pl->K * (int64_t)pl->esz))) return rc;
     ParamView pv{(const double*)params, pl->dp, pl->pcomplex};
     const int64_t tot = P * pl->K;
     if (pl->dtype == SAS_C128) {
       k_affine_coefs<cplx><<<(unsigned)((tot + 127) / 128), 128, 0, st>>>(pl->kind, pl->scale, pl->rate, pl->K, pv,
-                                                                          nullptr, P, (cplx*)pl->fco);
+                                                                          coef_table, P, (cplx*)pl->fco);
       k_resid_affine<cplx><<<grid, 256, 0, st>>>((const cplx*)pl->X, pl->n, pl->r, pl->K, pl->csr_rp_d,
                                                  pl->csr_ci_d, (const cplx* const*)pl->csr_va_d,
-                                                 (const cplx*)pl->fco, (const cplx*)pl->full_b,
+                                                 (const cplx*)pl->fco, (const cplx*)bvec, bstride,
                                                  (const cplx*)coef, pl->rpart);
     } else {
       k_affine_coefs<double><<<(unsigned)((tot + 127) / 128), 128, 0, st>>>(pl->kind, pl->scale, pl->rate, pl->K,
-                                                                            pv, nullptr, P, (double*)pl->fco);
+                                                                            pv, coef_table, P, (double*)pl->fco);
       k_resid_affine<double><<<grid, 256, 0, st>>>((const double*)pl->X, pl->n, pl->r, pl->K, pl->csr_rp_d,
                                                    pl->csr_ci_d, (const double* const*)pl->csr_va_d,
-                                                   (const double*)pl->fco, (const double*)pl->full_b,
+                                                   (const double*)pl->fco, (const double*)bvec, bstride,
                                                    (const double*)coef, pl->rpart);
     }
     pl->last_launches += 2;
@@ -1237,13 +1242,13 @@ extern "C" int sas_residual(sas_plan* pl, const void* params, const void* coef, 
     if ((rc = dalloc(&xs, (size_t)P * pl->n * sizeof(double)))) return rc;
     if ((rc = launch_lift_dmma(pl, (const double*)coef, P, xs, st))) { cudaFree(xs); return rc; }
     k_resid_gauss<<<grid, 256, 0, st>>>((const double*)pl->X, pl->n, pl->r, pl->pts, pl->pdim, pl->ridge, pl->dp,
-                                        (const double*)pl->full_b, (const double*)params, xs, pl->rpart);
+                                        (const double*)bvec, bstride, (const double*)params, xs, pl->rpart);
     cudaError_t e = cudaStreamSynchronize(st);
     cudaFree(xs);
     if (e != cudaSuccess) { sas_set_error("gauss residual: %s", cudaGetErrorString(e)); return SAS_ERR_CUDA; }
     pl->last_launches += 2;
   }
-  k_resid_finish<<<(unsigned)((P + 127) / 128), 128, 0, st>>>(pl->rpart, nb, P, relres);
+  k_resid_finish<<<(unsigned)((P + 127) / 128), 128, 0, st>>>(pl->rpart, nb, P, relres, floor_est);
   pl->last_launches++;
   SAS_CUDA_CHECK(cudaGetLastError());
   return SAS_OK;

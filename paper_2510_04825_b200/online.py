@@ -662,12 +662,17 @@ def lift_batch(plan: OnlinePlan, coefficients) -> np.ndarray:
 
 
 def set_full_operator(plan: OnlinePlan):
-    """Upload the full operator (for relative_residual)."""
+    """Upload the full operator (for relative_residual).  A p-dependent
+    right-hand side is passed per call instead (relative_residual)."""
     g = _gpu(plan)
     sysm = plan.system
-    b = np.ascontiguousarray(np.asarray(sysm.full_rhs(None) if g.rhs_constant else sysm.b).astype(g.np_dtype))
+    if g.rhs_constant:
+        b = np.asarray(sysm.full_rhs(None) if hasattr(sysm, "operator") else sysm.b)
+    else:
+        b = np.zeros(g.n)
+    b = np.ascontiguousarray(b.astype(g.np_dtype))
     keep = [b]
-    op = getattr(sysm, "operator", None)
+    op = row_operator(sysm)
     if sysm.affine_terms is not None:
         K = len(sysm.affine_terms)
         rps, cis, vas = (C.c_void_p * K)(), (C.c_void_p * K)(), (C.c_void_p * K)()
@@ -689,8 +694,12 @@ def set_full_operator(plan: OnlinePlan):
     g._operator_set = True
 
 
-def relative_residual(plan: OnlinePlan, parameters, coefficients) -> np.ndarray:
-    """||A(p) Q_X c - b|| / max(||b||, 1e-300) per parameter (cli.py:285, 344-351), on the GPU."""
+def relative_residual(plan: OnlinePlan, parameters, coefficients, return_floor: bool = False):
+    """||A(p) Q_X c - b(p)|| / max(||b(p)||, 1e-300) per parameter (cli.py:285,
+    344-351), on the GPU (sas_residual).  With return_floor, also the rounding
+    floor 100 eps || |A(p)| |x| || / ||b(p)||: a relative
+    residual below it is rounding noise.  Opaque affine coefficients and a
+    p-dependent right-hand side are evaluated on the host per parameter."""
     import torch
     g = _gpu(plan)
     if not g._operator_set:
@@ -699,10 +708,20 @@ def relative_residual(plan: OnlinePlan, parameters, coefficients) -> np.ndarray:
     dev = f"cuda:{g.device}"
     pt = torch.from_numpy(g.params_array(parameters)).to(dev)
     ct = torch.from_numpy(np.ascontiguousarray(np.asarray(coefficients).astype(g.np_dtype))).to(dev)
+    tab = g.coef_table(parameters)
+    tab_t = None if tab is None else torch.from_numpy(tab).to(dev)
+    b_t = None
+    if not g.rhs_constant:
+        rows = np.stack([np.asarray(plan.system.full_rhs(p)) for p in parameters]).astype(g.np_dtype)
+        b_t = torch.from_numpy(np.ascontiguousarray(rows)).to(dev)
     out = torch.empty(len(parameters), dtype=torch.float64, device=dev)
+    fl = torch.empty(len(parameters), dtype=torch.float64, device=dev)
     st = torch.cuda.current_stream(g.device)
-    _capi.check(g.lib.sas_residual(g.handle, _capi.ptr(pt), _capi.ptr(ct), len(parameters), _capi.ptr(out),
-                                   C.c_void_p(st.cuda_stream)), "sas_residual")
+    _capi.check(g.lib.sas_residual(g.handle, _capi.ptr(pt), _capi.ptr(ct), len(parameters), _capi.ptr(tab_t),
+                                   _capi.ptr(b_t), _capi.ptr(out), _capi.ptr(fl), C.c_void_p(st.cuda_stream)),
+                "sas_residual")
+    if return_floor:
+        return out.cpu().numpy(), fl.cpu().numpy()
     return out.cpu().numpy()
 
 
