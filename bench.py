@@ -413,7 +413,10 @@ def main():
     params_t = online.device_params(plan, my_params, device=dev)
     out = online.alloc_outputs(plan, Pl, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # 256 MiB > 126 MB L2
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated (non-default) stream: the solve's CUDA graph is captured and
+    # replayed on it directly; events, the L2 flush and copies go to it too
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
 
     for _ in range(W):
         online.solve_device(plan, params_t, out, stream)

@@ -158,3 +158,39 @@ def test_gauss_rows_every_column_tiling(r):
         floor = online_ref.ls_floor(m, t, sel.weights)
         d = np.linalg.norm(res.coefficients[k] - c) / np.linalg.norm(c)
         assert d <= max(1e-10, 10 * floor), (r, k, d, floor)
+
+
+@pytest.mark.parametrize("cfg,kw", [(1, dict(n=2000)), (2, dict(n=1000)), (3, dict(grid=40)), (4, dict(grid=40))])
+def test_graph_replay_matches_direct_launch(cfg, kw):
+    """sas_solve captures its second identical call into a CUDA graph and
+    replays it afterwards: the replayed results are bitwise those of the
+    direct launches, stage timing still reports every kernel, and a call with
+    other buffers drops back to direct launches."""
+    import torch
+    prob = problems.build(cfg, **kw)
+    basis, sel = offline(prob)
+    plan = online.precompute_online(prob.system, basis, sel)
+    params = prob.test_params(64)
+    pt = online.device_params(plan, params)
+    outs = []
+    for k in range(4):   # direct, capture, replay, replay
+        out = online.alloc_outputs(plan, len(params)) if k == 0 else outs[0]
+        n = online.solve_device(plan, pt, out)
+        torch.cuda.synchronize()
+        outs.append(out)
+        snap = {key: v.clone() for key, v in out.items()}
+        if k == 0:
+            first, n0 = snap, n
+        else:
+            assert n == n0
+            for key in ("coef", "sres", "status"):
+                assert torch.equal(snap[key], first[key]), (cfg, k, key)
+    plan.gpu.set_timing(True)
+    for _ in range(3):
+        online.solve_device(plan, pt, outs[0])
+        assert len(plan.gpu.stage_times()) >= 1
+    plan.gpu.set_timing(False)
+    other = online.alloc_outputs(plan, len(params))
+    online.solve_device(plan, pt, other)
+    torch.cuda.synchronize()
+    assert torch.equal(other["coef"], first["coef"])
