@@ -5,9 +5,12 @@
 // (64 nodes x r, staged in shared memory), B = C^T tile (r x 64 parameters),
 // one warp per 8 nodes x 64 parameters, K = r padded to 4.  The stencil
 // residual then runs on the materialised x in chunks of 64 parameters, stored
-// in 16-parameter blocks (k_resid_stencil_b16).
+// in kResidPB-parameter blocks (k_resid_stencil_blk).
 #pragma once
 #include "sas_common.cuh"
+#ifndef SAS_RESID_PB
+#define SAS_RESID_PB 64
+#endif
 
 __device__ __forceinline__ void dmma884_r(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -26,10 +29,10 @@ __host__ __device__ inline int lift_ld(int r) {
   return kp;
 }
 
-// grid = (ceil(n/64), ceil(P/64)); block 256.  Output x[p*n + i] (BLK16 =
-// false, the lift() layout) or x[((p / 16) n + i) 16 + p mod 16] (BLK16 = true,
-// the residual checker's layout: a node's values for 16 consecutive parameters
-// fill one aligned 128-byte line).
+// grid = (ceil(n/64), ceil(P/64)); block 256.  Output x[p*n + i] (BLK =
+// false, the lift() layout) or x[((p / PB) n + i) PB + p mod PB] (BLK = true,
+// the residual checker's layout, PB = kResidPB: a node's values for PB
+// consecutive parameters are contiguous).
 template <bool BLK16>
 __global__ void __launch_bounds__(256) k_lift_dmma(const double* __restrict__ X, int64_t n, int r,
                                                    const double* __restrict__ C, int64_t P,
@@ -65,8 +68,9 @@ __global__ void __launch_bounds__(256) k_lift_dmma(const double* __restrict__ X,
     for (int t = 0; t < 8; ++t) {
       const int64_t p = p0 + t * 8 + 2 * (lane & 3);
       if (BLK16) {
-        if (p < P) x[((p >> 4) * n + i) * 16 + (p & 15)] = acc[t][0];
-        if (p + 1 < P) x[(((p + 1) >> 4) * n + i) * 16 + ((p + 1) & 15)] = acc[t][1];
+        constexpr int PB = SAS_RESID_PB;
+        if (p < P) x[((p / PB) * n + i) * PB + (p % PB)] = acc[t][0];
+        if (p + 1 < P) x[(((p + 1) / PB) * n + i) * PB + ((p + 1) % PB)] = acc[t][1];
       } else {
         if (p < P) x[p * n + i] = acc[t][0];
         if (p + 1 < P) x[(p + 1) * n + i] = acc[t][1];
@@ -239,8 +243,14 @@ __global__ void k_resid_finish(const double* __restrict__ part, int nb, int64_t 
   if (floor_est) floor_est[p] = 100.0 * 2.220446049250313e-16 * sqrt(aa) / bn;
 }
 
-constexpr int kResidPB = 16;   // parameter values per pass: one 128-byte line of x per node
-constexpr int kResidTPN = 4;   // threads per node, kResidPB / kResidTPN parameter values each
+#ifndef SAS_RESID_PB
+#define SAS_RESID_PB 64
+#endif
+// parameter values per pass: a node's x values for them fill one aligned
+// 8 PB-byte block (64: one pass per 64-parameter chunk, so phi and the
+// neighbours are read once per chunk instead of once per 16 parameters)
+constexpr int kResidPB = SAS_RESID_PB;
+constexpr int kResidTPN = kResidPB / 4;   // threads per node, 4 parameter values each
 constexpr int kResidPT = kResidPB / kResidTPN;
 
 // Stencil residual for the 16 parameter values of pass blockIdx.y on the
@@ -254,8 +264,8 @@ constexpr int kResidPT = kResidPB / kResidTPN;
 // x_i and x_m are whole aligned 128-byte lines read by 8 lanes, the node's phi
 // and neighbour indices are broadcast loads serving 16 parameter values.
 // grid = (nb, passes); partial sums of |r|^2, |b|^2 and || |A| |x| ||^2 per CTA and parameter.
-__global__ void __launch_bounds__(256, 2) k_resid_stencil_b16(const double* __restrict__ x, int64_t n, int64_t P,
-                                                           const int64_t* __restrict__ nbr,
+__global__ void __launch_bounds__(256, 2) k_resid_stencil_blk(const double* __restrict__ x, int64_t n, int64_t P,
+                                                           const int32_t* __restrict__ nbr,
                                                            const double* __restrict__ phi, int E, int dp, double hh,
                                                            const double* __restrict__ b,
                                                            const double* __restrict__ params,
@@ -302,7 +312,7 @@ __global__ void __launch_bounds__(256, 2) k_resid_stencil_b16(const double* __re
       double phv[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) phv[k] = (k < dp) ? __ldg(ph + k) : 0.0;
-      const int64_t m = __ldg(nbr + i * E + e);
+      const int64_t m = __ldg(nbr + i * E + e);   // int32: n < 2^31
       double xm[kResidPT];
 #pragma unroll
       for (int h = 0; h < kResidPT / 2; ++h) {

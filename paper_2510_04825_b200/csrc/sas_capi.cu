@@ -159,7 +159,7 @@ struct sas_plan {
   double k3_dmax = 0.0;          // largest squared distance in exp table units (K3 fast-exp test)
   double* Xfrag = nullptr;  // K3 v3 fragment-ordered X^T
   // full operator for the residual checker
-  int64_t* full_nbr = nullptr;
+  int32_t* full_nbr = nullptr;  // n x E neighbours (int32: n < 2^31), -1 on Dirichlet edges
   double* full_phi = nullptr;
   void* full_b = nullptr;
   std::vector<int64_t*> csr_rp, csr_ci;
@@ -1188,7 +1188,7 @@ static int launch_lift_dmma(sas_plan* pl, const double* coef, int64_t P, double*
   for (int64_t p0 = 0; p0 < P; p0 += 65535LL * kLiftPar) {
     const int64_t pc = (P - p0 < 65535LL * kLiftPar) ? P - p0 : 65535LL * kLiftPar;
     dim3 grid((unsigned)((pl->n + kLiftNodes - 1) / kLiftNodes), (unsigned)((pc + kLiftPar - 1) / kLiftPar));
-    if (blk16)  // p0 is a multiple of 16: the blocks of this launch start at block p0 / 16
+    if (blk16)  // p0 is a multiple of kResidPB: the blocks of this launch start at block p0 / kResidPB
       k_lift_dmma<true><<<grid, 256, smem, st>>>((const double*)pl->X, pl->n, pl->r, coef + p0 * pl->r, pc,
                                                  x + p0 * pl->n);
     else
@@ -1237,7 +1237,12 @@ extern "C" int sas_plan_set_operator(sas_plan* pl, const int64_t* const* row_ptr
     if (pl->full_phi) cudaFree(pl->full_phi);
     pl->full_nbr = nullptr;
     pl->full_phi = nullptr;
-    if ((rc = dupload(&pl->full_nbr, nbr_full, (size_t)pl->n * pl->E * sizeof(int64_t)))) return rc;
+    ARG_CHECK(pl->n < (1ll << 31), "set_operator: stencil residual needs n < 2^31");
+    {
+      std::vector<int32_t> nb32((size_t)pl->n * pl->E);
+      for (size_t q = 0; q < nb32.size(); ++q) nb32[q] = (int32_t)nbr_full[q];
+      if ((rc = dupload(&pl->full_nbr, nb32.data(), nb32.size() * sizeof(int32_t)))) return rc;
+    }
     if ((rc = dupload(&pl->full_phi, phi_full, (size_t)pl->n * pl->E * pl->dp * sizeof(double)))) return rc;
   } else if (pl->op == SAS_OP_AFFINE) {
     ARG_CHECK(row_ptr && col && val, "set_operator: affine needs CSR arrays");
@@ -1296,7 +1301,7 @@ extern "C" int sas_residual(sas_plan* pl, const void* params, const void* coef, 
   const int64_t bstride = b_table ? pl->n : 0;
   if (pl->op == SAS_OP_STENCIL) {
     // x for a chunk of (up to) 64 parameters (K5, DMMA, one X pass per chunk),
-    // stored in 16-parameter blocks, then the stencil residual on it (K6)
+    // stored in kResidPB-parameter blocks, then the stencil residual on it (K6)
     ARG_CHECK(pl->full_nbr, "sas_residual: stencil operator not set");
     ARG_CHECK(!b_table, "sas_residual: stencil systems take the plan's constant right-hand side");
     const int64_t chunk = P < 64 ? ((P + kResidPB - 1) / kResidPB) * kResidPB : 64;
@@ -1305,7 +1310,7 @@ extern "C" int sas_residual(sas_plan* pl, const void* params, const void* coef, 
       const int64_t pc = (P - p0 < chunk) ? P - p0 : chunk;
       if ((rc = launch_lift_dmma(pl, (const double*)coef + p0 * pl->r, pc, pl->xscr, st, true))) return rc;
       dim3 g2(nb, (unsigned)((pc + kResidPB - 1) / kResidPB));
-      k_resid_stencil_b16<<<g2, 256, 0, st>>>(pl->xscr, pl->n, pc, pl->full_nbr, pl->full_phi, pl->E, pl->dp, pl->hh,
+      k_resid_stencil_blk<<<g2, 256, 0, st>>>(pl->xscr, pl->n, pc, pl->full_nbr, pl->full_phi, pl->E, pl->dp, pl->hh,
                                               (const double*)pl->full_b, (const double*)params + p0 * pl->dp,
                                               pl->rpart + p0 * nb * 3);
       pl->last_launches += 2;
