@@ -185,6 +185,7 @@ int32_t sas_last_launch_count(const sas_plan* plan);
  * and per-launch milliseconds with their stage ids (SAS_STAGE_*). */
 #define SAS_STAGE_LSQ 1        /* K4 batched least squares (+ fused assembly) */
 #define SAS_STAGE_GAUSS_ROWS 2 /* K3 Gaussian kernel-row contraction */
+#define SAS_STAGE_STENCIL_ROWS 3 /* K2 stencil-row assembly as its own launch (compact-WY path) */
 int sas_plan_set_timing(sas_plan* plan, int32_t enable);
 int32_t sas_stage_times(sas_plan* plan, float* ms, int32_t* stage, int32_t cap);
 

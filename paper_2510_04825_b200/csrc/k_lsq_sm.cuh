@@ -141,11 +141,11 @@ __host__ __device__ inline size_t lsq_sm_smem_bytes(int RA, int r, size_t scratc
 
 // Rank test, back substitution, sampled residual and output value from the
 // column-major factorisation (R_ij = A[j lda + i], i < j; y_i = A[r lda + i])
-// and the unweighted column-major M | t in mg (ldg = s).
+// and the unweighted column-major M | t in mg (column stride ldg).
 template <typename T>
 __device__ __forceinline__ void sm_finish(const LsqArgs<T>& a, int64_t p, const T* A, int lda, const T* mg,
                                           T* cvec, const T* rdiag, const double* nrm_s, double* rinfo,
-                                          double* red) {
+                                          double* red, int ldg) {
   using S = Sc<T>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int s = a.s, r = a.r;
@@ -202,13 +202,13 @@ __device__ __forceinline__ void sm_finish(const LsqArgs<T>& a, int64_t p, const 
     int j = 0;
     for (; j + 4 <= r; j += 4) {
 #pragma unroll
-      for (int t = 0; t < 4; ++t) a4[t] = S::add(a4[t], S::mul(mg[(size_t)(j + t) * s + i], cvec[j + t]));
+      for (int t = 0; t < 4; ++t) a4[t] = S::add(a4[t], S::mul(mg[(size_t)(j + t) * ldg + i], cvec[j + t]));
     }
 #pragma unroll
     for (int t = 0; t < 3; ++t)
-      if (j + t < r) a4[t] = S::add(a4[t], S::mul(mg[(size_t)(j + t) * s + i], cvec[j + t]));
+      if (j + t < r) a4[t] = S::add(a4[t], S::mul(mg[(size_t)(j + t) * ldg + i], cvec[j + t]));
     const T acc = S::add(S::add(a4[0], a4[1]), S::add(a4[2], a4[3]));
-    T res = S::sub(acc, mg[(size_t)r * s + i]);
+    T res = S::sub(acc, mg[(size_t)r * ldg + i]);
     if (a.w) res = S::mulr(res, a.w[i]);
     ss += S::abs2(res);
   }
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(32 * W, MINB) k_lsq_sm(LsqArgs<T> a, Asm as, T
       __syncthreads();
     }
     SM_PROF_MARK(2);
-    sm_finish<T>(a, p, A, lda, mg, cvec, rdiag, nrm_s, rinfo, red);
+    sm_finish<T>(a, p, A, lda, mg, cvec, rdiag, nrm_s, rinfo, red, s);
     SM_PROF_MARK(3);
   }
 #ifdef SAS_SM_PROF

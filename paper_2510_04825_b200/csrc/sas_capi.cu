@@ -20,6 +20,7 @@
 #include "k_lsq_mw.cuh"
 #include "k_lsq_cw.cuh"
 #include "k_lsq_sm.cuh"
+#include "k_lsq_wy.cuh"
 #include "k_tsqr.cuh"
 #include "k_cg.cuh"
 #include "k_gauss.cuh"
@@ -171,6 +172,8 @@ struct sas_plan {
   double* Mscr = nullptr;
   double* cw_mg = nullptr;   // K4 column-owner kernel (PARK): per-CTA slots for the unweighted M
   int64_t cw_mg_n = 0;
+  double* wy_mg = nullptr;   // K4 compact-WY kernel: [M | t] blocks of a parameter chunk (k_wy_stencil_rows)
+  int64_t wy_mg_n = 0;
   int64_t Mscr_P = 0;
   double* rpart = nullptr;
   int64_t rpart_n = 0;
@@ -289,7 +292,7 @@ static void plan_free(sas_plan* pl) {
   DevGuard g(pl->device);
   void* ptrs[] = {pl->X, pl->S, pl->w, pl->t, pl->proj, pl->kind, pl->scale, pl->rate, pl->blocks,
                   pl->phi, pl->G, pl->gmap, pl->pts, pl->D, pl->Dfrag, pl->Xfrag, pl->full_nbr, pl->full_phi, pl->full_b,
-                  pl->csr_rp_d, pl->csr_ci_d, pl->csr_va_d, pl->Mscr, pl->cw_mg, pl->rpart, pl->xscr, pl->fco,
+                  pl->csr_rp_d, pl->csr_ci_d, pl->csr_va_d, pl->Mscr, pl->cw_mg, pl->wy_mg, pl->rpart, pl->xscr, pl->fco,
                   pl->h_params, pl->h_ctab, pl->h_rhs, pl->h_coef, pl->h_sres, pl->h_outv,
                   pl->h_status, pl->h_bad};
   for (void* p : ptrs)
@@ -817,6 +820,82 @@ static bool lsq_force_cta() {
   return v == 1;
 }
 
+// Compact-WY blocked Householder on DMMA (k_lsq_wy) for the real stencil
+// shapes with 33 <= r+1 <= 56 and s <= 224 (configs 3 and 5): the sweep runs
+// in chunks, each chunk's [M | t] blocks assembled by k_wy_stencil_rows into
+// plan scratch and factored by k_lsq_wy.  SAS_LSQ_WY=off disables it (the
+// column-owner kernel then takes these shapes), SAS_LSQ_WY_CHUNK=<p> sets the
+// chunk (default: 1.5 GB of blocks).
+static int lsq_wy_env() {
+  static int v = -3;
+  if (v == -3) {
+    const char* e = getenv("SAS_LSQ_WY");
+    v = !e ? -1 : (strcmp(e, "off") == 0 ? 0 : 1);
+  }
+  return v;
+}
+template <int RA, int W, int MINB, int NTM>
+static int launch_lsq_wy_t(sas_plan* pl, const LsqArgs<double>& a, const double* mg, int ld, int cpad,
+                           cudaStream_t st) {
+  const size_t smem = lsq_wy_smem_bytes(ld, cpad);
+  auto kern = k_lsq_wy<RA, W, MINB, NTM>;
+  SMEM_OPTIN(k_lsq_wy<RA, W, MINB, NTM>);
+  int occ = 0;
+  SAS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * W, smem));
+  if (occ < 1) {
+    sas_set_error("least-squares kernel does not fit (s=%d r=%d smem=%zu)", a.s, a.r, smem);
+    return SAS_ERR_ARG;
+  }
+  int64_t grid = (int64_t)occ * pl->sms;
+  if (grid > a.P) grid = a.P;
+  if (grid < 1) grid = 1;
+  stage_begin(pl, st, SAS_STAGE_LSQ);
+  kern<<<(unsigned)grid, 32 * W, smem, st>>>(a, mg, ld, cpad);
+  stage_end(pl, st);
+  SAS_CUDA_CHECK(cudaGetLastError());
+  pl->last_launches++;
+  return SAS_OK;
+}
+// returns -1 when the shape is not covered
+static int try_lsq_wy_stencil(sas_plan* pl, const LsqArgs<double>& a, const AsmStencil& as, cudaStream_t st) {
+  if (lsq_wy_env() == 0 || lsq_force_cta()) return -1;
+  if (lsq_wy_env() < 0 && (lsq_sm_env() == 1 || lsq_cw_env() >= 0)) return -1;  // another kernel was asked for
+  const int cols = a.r + 1, s = a.s;
+  if (cols < (lsq_wy_env() == 1 ? 9 : 33) || cols > 56 || s > 224 || s < a.r || as.E + 1 > 8) return -1;
+  const int ld = wy_ld(s), cpad = wy_cpad(a.r);
+  const int64_t blk = (int64_t)ld * cpad * (int64_t)sizeof(double);
+  int64_t chunk = (3ll << 29) / blk;
+  if (const char* e = getenv("SAS_LSQ_WY_CHUNK")) chunk = atoll(e);
+  if (chunk < 1) chunk = 1;
+  if (chunk > a.P) chunk = a.P;
+  if (chunk > 65535ll * kWyPB) chunk = 65535ll * kWyPB;
+  int rc = ensure(&pl->wy_mg, &pl->wy_mg_n, chunk * blk);
+  if (rc) return rc;
+  const size_t rsmem = wy_rows_smem_bytes(as.E + 1, a.r);
+  if (int rc2 = smem_optin<k_wy_stencil_rows>(false)) return rc2;
+  for (int64_t p0 = 0; p0 < a.P; p0 += chunk) {
+    const int64_t pc = (a.P - p0 < chunk) ? (a.P - p0) : chunk;
+    dim3 grid((unsigned)(ld / kWyRB), (unsigned)((pc + kWyPB - 1) / kWyPB));
+    stage_begin(pl, st, SAS_STAGE_STENCIL_ROWS);
+    k_wy_stencil_rows<<<grid, 256, rsmem, st>>>(as.E, as.dp, as.phi, as.G, as.gmap, as.hh, as.params + p0 * as.dp,
+                                                a.t + p0 * a.t_stride, a.t_stride, pc, s, a.r, ld, cpad, pl->wy_mg);
+    stage_end(pl, st);
+    SAS_CUDA_CHECK(cudaGetLastError());
+    pl->last_launches++;
+    LsqArgs<double> b = a;
+    b.P = pc;
+    b.coef = a.coef + p0 * a.r;
+    b.sres = a.sres + p0;
+    b.outv = a.outv ? a.outv + 2 * p0 : nullptr;
+    b.status = a.status + p0;
+    b.badcol = a.badcol ? a.badcol + p0 : nullptr;
+    if (s <= 160) rc = launch_lsq_wy_t<5, 8, 2, 6>(pl, b, pl->wy_mg, ld, cpad, st);
+    else rc = launch_lsq_wy_t<7, 8, 2, 6>(pl, b, pl->wy_mg, ld, cpad, st);
+    if (rc) return rc;
+  }
+  return SAS_OK;
+}
+
 // Kernel choice for the batched least squares: k_lsq_mw<RG, RA, CB, W> holds
 // [M_w | t_w] in registers, W warps per parameter value, an (RG row groups x
 // 32/RG column groups) lane layout and RA x CB slots per lane, so it covers
@@ -997,6 +1076,8 @@ static int solve_t(sas_plan* pl, const void* params, int64_t P, const double* co
     case SAS_OP_STENCIL: {
       if constexpr (std::is_same<T, double>::value) {
         AsmStencil as{pl->E, pl->dp, pl->phi, pl->G, pl->gmap, pl->hh, (const double*)params};
+        const int rcw = try_lsq_wy_stencil(pl, a, as, st);
+        if (rcw >= 0) return rcw;
         return launch_lsq<double>(pl, a, as, AsmStencil::scratch_bytes(pl->s, pl->E), st);
       }
       sas_set_error("stencil: complex not supported");
