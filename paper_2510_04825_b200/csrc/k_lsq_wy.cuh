@@ -61,7 +61,7 @@ constexpr int kWyRB = 8;
 constexpr int kWyPB = 32;
 
 __host__ __device__ inline size_t wy_rows_smem_bytes(int E1, int r) {
-  return ((size_t)kWyRB * E1 * r + 1) / 2 * 2 * sizeof(double) + (size_t)kWyPB * kWyRB * 8 * sizeof(double);
+  return ((size_t)kWyRB * E1 * r + 1) / 2 * 2 * sizeof(double) + 2 * (size_t)kWyPB * kWyRB * 8 * sizeof(double);
 }
 
 __global__ void __launch_bounds__(256)
@@ -72,7 +72,8 @@ k_wy_stencil_rows(int E, int dp, const double* __restrict__ phi, const double* _
   extern __shared__ __align__(16) unsigned char wy_rows_smem[];
   const int E1 = E + 1;
   double* Gs = reinterpret_cast<double*>(wy_rows_smem);
-  double* cs = Gs + ((size_t)kWyRB * E1 * r + 1) / 2 * 2;
+  double* cs = Gs + ((size_t)kWyRB * E1 * r + 1) / 2 * 2;   // [pl][q / 2][row] double2: conflict-free reads below
+  double* ce = cs + (size_t)kWyPB * kWyRB * 8;               // [pl][row][edge] edge coefficients
   const int tid = threadIdx.x;
   const int i0 = blockIdx.x * kWyRB;
   const int64_t p0 = (int64_t)blockIdx.y * kWyPB;
@@ -92,14 +93,14 @@ k_wy_stencil_rows(int E, int dp, const double* __restrict__ phi, const double* _
     const double* pp = params + (p0 + pl) * dp;
     double arg = dmul_exact(pp[0], ph[0]);
     for (int k = 1; k < dp; ++k) arg = dadd_exact(arg, dmul_exact(pp[k], ph[k]));
-    cs[(pl * kWyRB + i) * 8 + 1 + e] = exp(arg) / hh;
+    ce[(pl * kWyRB + i) * 8 + e] = exp(arg) / hh;
   }
   __syncthreads();
   // per (parameter value, row): the diagonal (edge order), then the signed
   // coefficient of every gathered row
   for (int idx = tid; idx < np * nrows; idx += 256) {
     const int pl = idx / nrows, i = idx - pl * nrows;
-    double* ci = cs + (pl * kWyRB + i) * 8;
+    const double* ci = ce + (pl * kWyRB + i) * 8 - 1;   // ci[1 + e]: edge e
     double d = 0.0;
     for (int e = 0; e < E; ++e) d = dadd_exact(d, ci[1 + e]);
     const int8_t* mp = gmap + (i0 + i) * E1;
@@ -110,7 +111,7 @@ k_wy_stencil_rows(int E, int dp, const double* __restrict__ phi, const double* _
       nv[q] = (slot < 0) ? 0.0 : (slot == 0 ? d : -ci[slot]);
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) ci[q] = nv[q];
+    for (int q = 0; q < 8; ++q) cs[((pl * 4 + (q >> 1)) * kWyRB + i) * 2 + (q & 1)] = nv[q];
   }
   __syncthreads();
   // products: thread = (row i, column pair), the gathered rows of its two
@@ -128,10 +129,10 @@ k_wy_stencil_rows(int E, int dp, const double* __restrict__ phi, const double* _
   for (int pl = 0; pl < np; ++pl) {
     double m0 = 0.0, m1 = 0.0;
     if (rok) {
-      const double2* c2 = reinterpret_cast<const double2*>(cs + (pl * kWyRB + i) * 8);
+      const double2* c2 = reinterpret_cast<const double2*>(cs) + pl * 4 * kWyRB + i;
 #pragma unroll
       for (int q2 = 0; q2 < 4; ++q2) {
-        const double2 c = c2[q2];
+        const double2 c = c2[q2 * kWyRB];
         if (2 * q2 < E1) {
           m0 = fma(c.x, g0[2 * q2], m0);
           m1 = fma(c.x, g1[2 * q2], m1);
@@ -152,80 +153,193 @@ k_wy_stencil_rows(int E, int dp, const double* __restrict__ phi, const double* _
 }
 
 // ---------------------------------------------------------------------------
+constexpr int kWyWarps = 8;        // warps 0..3 factor panels, all eight run the DMMA phases
+constexpr int kWyPanelWarps = 4;
+
 __host__ __device__ inline size_t lsq_wy_smem_bytes(int ld, int cpad) {
-  // A, W partials (2 x 8 x cpad), Z (8 x cpad), weights, tau/R_kk/|R_kk|/c (64 each),
-  // residual partials (32), rank info (2), mbarrier
-  return ((size_t)ld * cpad + 24 * (size_t)cpad + ld + 4 * 64 + 32 + 2) * sizeof(double) + 16;
+  // A (reused for the residual's per-warp row partials, kWyWarps x ld <= ld x cpad);
+  // W partials (2 x 8 x cpad) + Z (8 x cpad); weights (ld); tau / R_kk / |R_kk| / c
+  // (cpad each), residual partials (8), rank info (2), mbarrier
+  return ((size_t)ld * cpad + 24 * (size_t)cpad + ld + 4 * (size_t)cpad + 8 + 2) * sizeof(double) + 16;
 }
 
-// Panel j: unblocked Householder on columns [8j, 8j+8) by one warp.  Lane l
-// holds rows l + 32u of a column.  Reflector columns are k < r; the remaining
-// panel columns (t, zero padding) are only updated.
-template <int RA>
-__device__ __forceinline__ void wy_panel(double* A, int ld, int s, int r, int j, int lane, double* tau_s,
-                                         double* rdiag, double* nrm_s) {
-  const int k0 = 8 * j, cend = k0 + 8;
-  const int kend = (cend < r) ? cend : r;
-  for (int k = k0; k < kend; ++k) {
-    double* colk = A + (size_t)k * ld;
-    double v[RA];
-    double ss = 0.0;
-#pragma unroll
-    for (int u = 0; u < RA; ++u) {
-      const int i = lane + 32 * u;
-      const double x = (i < s) ? colk[i] : 0.0;
-      v[u] = (i >= k) ? x : 0.0;
-      ss += v[u] * v[u];
-    }
-    ss = warp_allreduce_d(ss);
-    double al = 0.0;
-#pragma unroll
-    for (int u = 0; u < RA; ++u)
-      if (u == (k >> 5)) al = v[u];
-    const double alpha = __shfl_sync(0xffffffffu, al, k & 31);
+__device__ __forceinline__ void wy_bar_panel() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+
+// Panel j: unblocked Householder on columns [8j, 8j+8), column-parallel over the
+// four panel warps: warp g holds columns g and g+4 in registers (lane l: rows
+// l + 32u).  Step k: the owner of column k forms the reflector (|x| from the
+// norm carried over from the previous step) and writes the column - V in place,
+// head on the diagonal - and tau to shared memory; after ONE named barrier the
+// four warps read v and reflect their remaining columns, each with one warp
+// reduction.  The owner of the next pivot column reduces q = |y_{k+1}[k:]|^2
+// together with its dot product: the reflection preserves q, so the next norm
+// below row k is q - y_{k+1,k}^2 (as exact as a direct sum unless one
+// reflection removes most of the column; then it is summed directly).
+// Reflector columns are k < r; the remaining panel columns (t, zero padding)
+// are only updated.
+template <int RA, int KK>
+__device__ __forceinline__ void wy_panel_step(double (&y)[2][RA], double& ss, double* A, int ld, int s, int k0, int r,
+                                              int g, int lane, const bool (&inb)[RA], double* tau_s, double* rdiag,
+                                              double* nrm_s) {
+  constexpr int OWN = KK & 3, SL = KK >> 2;
+  const int k = k0 + KK;
+  if (k >= r) return;   // uniform over the panel warps
+  double* colk = A + k * ld + k0 + lane;   // row k0 + lane + 32u at colk[32u]
+  if (g == OWN) {
+    const double alpha = __shfl_sync(0xffffffffu, y[SL][0], KK);   // row k: lane KK, slot 0
     const double nrm = sqrt(ss);
     const double aa = fabs(alpha);
     double beta = 0.0, tau = 0.0;
     if (nrm != 0.0) {
       beta = (aa == 0.0) ? -nrm : copysign(nrm, -alpha);   // -sign(x_k) |x|
-      tau = rcp_nr(nrm * (nrm + aa));
+      tau = rcp_nr(fma(nrm, aa, ss));                      // 1 / (|x| (|x| + |x_k|)), |x|^2 = ss
     }
     const double vhead = alpha - beta;
+    if (lane == KK) y[SL][0] = vhead;   // R above (lanes < KK), head, v below
 #pragma unroll
     for (int u = 0; u < RA; ++u)
-      if (lane + 32 * u == k) {
-        v[u] = vhead;
-        colk[k] = vhead;   // V in place: the head on the diagonal, R_kk in rdiag
-      }
+      if (inb[u]) colk[32 * u] = y[SL][u];
     if (lane == 0) {
       tau_s[k] = tau;
       rdiag[k] = beta;
       nrm_s[k] = nrm;
     }
-    for (int c = k + 1; c < cend; c += 4) {
-      double y[4][RA];
+  }
+  wy_bar_panel();
+  if constexpr (KK < 7) {
+    constexpr int NOWN = (KK + 1) & 3, NSL = (KK + 1) >> 2;
+    const bool act0 = g > KK, act1 = g + 4 > KK, nxt = g == NOWN;
+    if (!act1) return;   // both of this warp's columns are finished (act0 implies act1)
+    const double tau = tau_s[k];
+    double v[RA];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const double* col = A + (size_t)(c + q) * ld;
+    for (int u = 0; u < RA; ++u) v[u] = inb[u] ? colk[32 * u] : 0.0;
+    if (lane < KK) v[0] = 0.0;   // rows k0 .. k-1 of column k are R entries
+    double d0 = 0.0, d1 = 0.0, q = 0.0;
 #pragma unroll
-        for (int u = 0; u < RA; ++u) {
-          const int i = lane + 32 * u;
-          y[q][u] = (c + q < cend && i < s) ? col[i] : 0.0;
-        }
+    for (int u = 0; u < RA; ++u) {
+      d0 = fma(v[u], y[0][u], d0);
+      d1 = fma(v[u], y[1][u], d1);
+    }
+    if (nxt) {
+      const double y0 = (lane >= KK) ? y[NSL][0] : 0.0;
+      q = y0 * y0;
+#pragma unroll
+      for (int u = 1; u < RA; ++u) q = fma(y[NSL][u], y[NSL][u], q);
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        d0 += __shfl_xor_sync(0xffffffffu, d0, off);
+        d1 += __shfl_xor_sync(0xffffffffu, d1, off);
+        q += __shfl_xor_sync(0xffffffffu, q, off);
       }
-      sm_apply<double, RA, 4>(y, v, tau);
+    } else {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        double* col = A + (size_t)(c + q) * ld;
+      for (int off = 16; off > 0; off >>= 1) {
+        d0 += __shfl_xor_sync(0xffffffffu, d0, off);
+        d1 += __shfl_xor_sync(0xffffffffu, d1, off);
+      }
+    }
+    const double w0 = act0 ? tau * d0 : 0.0, w1 = tau * d1;
 #pragma unroll
-        for (int u = 0; u < RA; ++u) {
-          const int i = lane + 32 * u;
-          if (c + q < cend && i < s) col[i] = y[q][u];
-        }
+    for (int u = 0; u < RA; ++u) {
+      y[0][u] = fma(-w0, v[u], y[0][u]);
+      y[1][u] = fma(-w1, v[u], y[1][u]);
+    }
+    if (nxt) {
+      const double e = __shfl_sync(0xffffffffu, y[NSL][0], KK);   // row k of the next pivot column, reflected
+      double ssn = fma(-e, e, q);
+      if (!(ssn > 0.25 * q)) {
+        const double y0 = (lane > KK) ? y[NSL][0] : 0.0;
+        ssn = y0 * y0;
+#pragma unroll
+        for (int u = 1; u < RA; ++u) ssn = fma(y[NSL][u], y[NSL][u], ssn);
+        ssn = warp_allreduce_d(ssn);
+      }
+      ss = ssn;
+    }
+  }
+}
+
+// The panel warps hold the rows at and below the panel's first row only:
+// lane l, slot u = row 8j + l + 32u (rows above are finished R rows), so the
+// pivot row of step KK is lane KK, slot 0 at compile time.
+template <int RA>
+__device__ __forceinline__ void wy_panel(double* A, int ld, int s, int r, int j, int g, int lane, double* tau_s,
+                                         double* rdiag, double* nrm_s) {
+  const int k0 = 8 * j;
+  bool inb[RA];
+#pragma unroll
+  for (int u = 0; u < RA; ++u) inb[u] = k0 + lane + 32 * u < s;
+  double y[2][RA];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const double* col = A + (k0 + g + 4 * c) * ld + k0 + lane;
+#pragma unroll
+    for (int u = 0; u < RA; ++u) y[c][u] = inb[u] ? col[32 * u] : 0.0;
+  }
+  double ss = 0.0;
+  if (g == 0) {
+#pragma unroll
+    for (int u = 0; u < RA; ++u) ss = fma(y[0][u], y[0][u], ss);
+    ss = warp_allreduce_d(ss);
+  }
+  wy_panel_step<RA, 0>(y, ss, A, ld, s, k0, r, g, lane, inb, tau_s, rdiag, nrm_s);
+  wy_panel_step<RA, 1>(y, ss, A, ld, s, k0, r, g, lane, inb, tau_s, rdiag, nrm_s);
+  wy_panel_step<RA, 2>(y, ss, A, ld, s, k0, r, g, lane, inb, tau_s, rdiag, nrm_s);
+  wy_panel_step<RA, 3>(y, ss, A, ld, s, k0, r, g, lane, inb, tau_s, rdiag, nrm_s);
+  wy_panel_step<RA, 4>(y, ss, A, ld, s, k0, r, g, lane, inb, tau_s, rdiag, nrm_s);
+  wy_panel_step<RA, 5>(y, ss, A, ld, s, k0, r, g, lane, inb, tau_s, rdiag, nrm_s);
+  wy_panel_step<RA, 6>(y, ss, A, ld, s, k0, r, g, lane, inb, tau_s, rdiag, nrm_s);
+  wy_panel_step<RA, 7>(y, ss, A, ld, s, k0, r, g, lane, inb, tau_s, rdiag, nrm_s);
+  // columns that were no pivots (t, padding: k >= r) go back updated; tau = 0 for them
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const int kc = k0 + g + 4 * c;
+    if (kc >= r) {
+      double* col = A + kc * ld + k0 + lane;
+#pragma unroll
+      for (int u = 0; u < RA; ++u)
+        if (inb[u]) col[32 * u] = y[c][u];
+      if (lane == 0) tau_s[kc] = 0.0;
+    }
+  }
+}
+
+// S3: A_trail -= V Z on column tiles [ti0, ti0 + ntile) after the panel, as
+// A^T += (-Z)^T V^T, for the 8-row tiles rt = j + vw0, j + vw0 + stride, ...
+template <int NTM>
+__device__ __forceinline__ void wy_s3(double* A, const double* Zs, int ld, int cpad, int rtn, int j, int ti0,
+                                      int ntile, int vw0, int stride, int lq, int lr) {
+  if (ntile <= 0) return;
+  double za[NTM][2];
+#pragma unroll
+  for (int ti = 0; ti < NTM; ++ti) {
+    const bool ok = ti < ntile;
+    const int cc = 8 * (j + 1 + ti0 + ti) + lq;
+    za[ti][0] = ok ? Zs[lr * cpad + cc] : 0.0;
+    za[ti][1] = ok ? Zs[(lr + 4) * cpad + cc] : 0.0;
+  }
+  const double* v0 = A + (8 * j + lr) * ld + lq;
+  const double* v1 = v0 + 4 * ld;
+  double* cb0 = A + (8 * (j + 1 + ti0) + lq) * ld + 2 * lr;
+  for (int rt = j + vw0; rt < rtn; rt += stride) {
+    double b0 = v0[8 * rt], b1 = v1[8 * rt];
+    if (rt == j) {
+      b0 = (lq >= lr) ? b0 : 0.0;
+      b1 = (lq >= lr + 4) ? b1 : 0.0;
+    }
+    double* cbase = cb0 + 8 * rt;
+#pragma unroll
+    for (int ti = 0; ti < NTM; ++ti) {
+      if (ti < ntile) {
+        double2* cp = reinterpret_cast<double2*>(cbase + 8 * ti * ld);
+        double2 c = *cp;
+        dmma884(c.x, c.y, za[ti][0], b0);
+        dmma884(c.x, c.y, za[ti][1], b1);
+        *cp = c;
       }
     }
   }
-  for (int k = kend + lane; k < cend; k += 32) tau_s[k] = 0.0;
 }
 
 #ifdef SAS_WY_PROF
@@ -234,92 +348,119 @@ __device__ __forceinline__ void wy_panel(double* A, int ld, int s, int r, int j,
 #define WY_PROF_MARK(ph) do {} while (0)
 #endif
 
-// One CTA of W warps per parameter value (persistent over p); s <= 32 RA rows,
-// r + 1 <= 8 NTM columns.  Mg: P blocks of ld x cpad doubles (k_wy_stencil_rows).
-template <int RA, int W, int MINB, int NTM>
-__global__ void __launch_bounds__(32 * W, MINB)
+// One CTA of eight warps per parameter value (persistent over p); s <= 32 RA rows,
+// r + 1 <= 8 (NTM + 1) columns.  Mg: P blocks of ld x cpad doubles (k_wy_stencil_rows).
+// Per panel: S1 (all warps) | S2 | S3 on the next panel's column tile (all warps) |
+// warps 0..3 factor the next panel while warps 4..7 finish S3 (look-ahead).
+template <int RA, int MINB, int NTM>
+__global__ void __launch_bounds__(32 * kWyWarps, MINB)
 k_lsq_wy(LsqArgs<double> a, const double* __restrict__ Mg, int ld, int cpad) {
+  constexpr int W = kWyWarps;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int s = a.s, r = a.r;
   const int nt = cpad >> 3, rtn = ld >> 3;
   double* A = reinterpret_cast<double*>(smem_raw);
-  double* Wp = A + (size_t)ld * cpad;
-  double* Zs = Wp + 16 * cpad;
-  double* ws = Zs + 8 * cpad;
+  double* Wp = A + ld * cpad;                // 2 x 8 x cpad
+  double* Zs = Wp + 16 * cpad;               // 8 x cpad
+  double* ws = Zs + 8 * cpad;                // weights (1 when unweighted), ld
   double* tau_s = ws + ld;
-  double* rdiag = tau_s + 64;
-  double* nrm_s = rdiag + 64;
-  double* cvec = nrm_s + 64;
-  double* red = cvec + 64;
-  double* rinfo = red + 32;
+  double* rdiag = tau_s + cpad;
+  double* nrm_s = rdiag + cpad;
+  double* cvec = nrm_s + cpad;
+  double* red = cvec + cpad;
+  double* rinfo = red + 8;
   uint64_t* bar = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(rinfo + 2) + 7) & ~(uintptr_t)7);
-  for (int i = tid; i < ld; i += 32 * W) ws[i] = (i < s) ? (a.w ? a.w[i] : 1.0) : 0.0;
-  if (tid == 0) {
-    mbar_init(bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
   const unsigned bytes = (unsigned)((size_t)ld * cpad * sizeof(double));
   const int64_t blk = (int64_t)ld * cpad;
   const int npanel = (r + 7) >> 3;
   const int lq = lane >> 2, lr = lane & 3;
+  const int n2 = ld >> 1;
+  const double qnan = __longlong_as_double(0x7ff8000000000000ll);
+  for (int i = tid; i < ld; i += 32 * W) ws[i] = (a.w && i < s) ? a.w[i] : 1.0;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    if ((int64_t)blockIdx.x < a.P) {
+      mbar_expect_tx(bar, bytes);
+      bulk_g2s(A, Mg + (int64_t)blockIdx.x * blk, bytes, bar);
+    }
+  }
+  __syncthreads();
   unsigned phase = 0;
 #ifdef SAS_WY_PROF
-  long long wy_tp[6] = {0, 0, 0, 0, 0, 0}, wy_t0 = clock64(), wy_t1;
+  long long wy_tp[8] = {0, 0, 0, 0, 0, 0, 0, 0}, wy_t0 = clock64(), wy_t1;
 #endif
 
   for (int64_t p = blockIdx.x; p < a.P; p += gridDim.x) {
     const double* mg = Mg + p * blk;
-    if (tid == 0) {
-      // the previous parameter value's generic-proxy accesses to A are ordered
-      // before the async-proxy write by the barrier that ended its finish
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      mbar_expect_tx(bar, bytes);
-      bulk_g2s(A, mg, bytes, bar);
-      if (p + gridDim.x < a.P)
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(mg + (int64_t)gridDim.x * blk), "r"(bytes)
-                     : "memory");
-    }
+    // the next parameter value's block: issued as soon as A is dead (after the
+    // residual's row partials, which reuse A, are summed; all generic-proxy accesses to
+    // A are ordered before the async-proxy write by the preceding barrier and the
+    // proxy fence)
+    auto issue_next = [&]() {
+      if (tid == 0 && p + gridDim.x < a.P) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_expect_tx(bar, bytes);
+        bulk_g2s(A, mg + (int64_t)gridDim.x * blk, bytes, bar);
+        if (p + 2 * (int64_t)gridDim.x < a.P)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(mg + 2 * (int64_t)gridDim.x * blk),
+                       "r"(bytes)
+                       : "memory");
+      }
+    };
     mbar_wait(bar, phase);
     phase ^= 1u;
     WY_PROF_MARK(0);
-    // weights in place, non-finite test (linalg.py:36-37, 102-105)
+    // weights in place, non-finite test (linalg.py:36-37, 102-105): lane = row pairs
+    // lane + 32m, warp = columns warp + W q.  Branch-free: an exponent field of all
+    // ones (inf / nan) carries into the sign bit of badbits.
     bool bad = false;
     {
-      const int n2 = ld >> 1;
+      double wr[8];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int i = 2 * (lane + 32 * m);
+        wr[2 * m] = (i < ld) ? ws[i] : 1.0;
+        wr[2 * m + 1] = (i < ld) ? ws[i + 1] : 1.0;
+      }
+      unsigned badbits = 0u;
       for (int jc = warp; jc <= r; jc += W) {
-        double2* col = reinterpret_cast<double2*>(A + (size_t)jc * ld);
-        for (int i2 = lane; i2 < n2; i2 += 32) {
-          double2 m = col[i2];
-          if (jc < r && !(isfinite(m.x) && isfinite(m.y))) bad = true;
-          if (a.w) {
-            m.x *= ws[2 * i2];
-            m.y *= ws[2 * i2 + 1];
-            col[i2] = m;
-          }
+        double2* col = reinterpret_cast<double2*>(A + jc * ld);
+        const unsigned live = (jc < r) ? 0x7ff00000u : 0u;   // t is not tested (the reference tests M only)
+        double2 mv[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) mv[m] = (lane + 32 * m < n2) ? col[lane + 32 * m] : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          badbits |= (((unsigned)__double2hiint(mv[m].x) & live) + 0x00100000u) |
+                     (((unsigned)__double2hiint(mv[m].y) & live) + 0x00100000u);
+          if (lane + 32 * m < n2) col[lane + 32 * m] = make_double2(mv[m].x * wr[2 * m], mv[m].y * wr[2 * m + 1]);
         }
       }
+      bad = (badbits >> 31) != 0u;
     }
     if (__syncthreads_or(bad)) {
       lsq_nonfinite<double>(a, p);
+      issue_next();
       continue;
     }
     WY_PROF_MARK(1);
+    if (warp < kWyPanelWarps) wy_panel<RA>(A, ld, s, r, 0, warp, lane, tau_s, rdiag, nrm_s);
+    __syncthreads();
+    WY_PROF_MARK(2);
 
     for (int j = 0; j < npanel; ++j) {
-      if (warp == 0) wy_panel<RA>(A, ld, s, r, j, lane, tau_s, rdiag, nrm_s);
-      __syncthreads();
-      WY_PROF_MARK(2);
       const int ntrail = nt - 1 - j;
       if (ntrail <= 0) break;
-      // S1: W = V^T [V | A_trail], two K halves (even / odd 8-row tiles) per column tile
+      // S1: W = V^T [V | A_trail]: units (column tile, K half), K half ks = the 8-row
+      // tiles j + ks, j + ks + 2, ...; the two halves are summed in S2
       {
-        const double* vcol = A + (size_t)(8 * j + lq) * ld + 2 * lr;
+        const double* vcol = A + (8 * j + lq) * ld + 2 * lr;
         const bool m0 = 2 * lr >= lq, m1 = 2 * lr + 1 >= lq;   // lower triangle of the diagonal tile
         for (int u = warp; u < 2 * (ntrail + 1); u += W) {
-          const int ti = u >> 1, ks = u & 1, ct = j + ti;
-          const double* acol = A + (size_t)(8 * ct + lq) * ld + 2 * lr;
+          const int ti = u >> 1, ks = u & 1;
+          const double* acol = vcol + 8 * ti * ld;
           double c0a = 0.0, c1a = 0.0, c0b = 0.0, c1b = 0.0;
           int rt = j + ks;
           if (ks == 0) {
@@ -327,22 +468,19 @@ k_lsq_wy(LsqArgs<double> a, const double* __restrict__ Mg, int ld, int cpad) {
             double2 av = *reinterpret_cast<const double2*>(acol + 8 * rt);
             vv.x = m0 ? vv.x : 0.0;
             vv.y = m1 ? vv.y : 0.0;
-            if (ti == 0) {
-              av.x = m0 ? av.x : 0.0;
-              av.y = m1 ? av.y : 0.0;
-            }
+            if (ti == 0) av = vv;
             dmma884(c0a, c1a, vv.x, av.x);
             dmma884(c0b, c1b, vv.y, av.y);
             rt += 2;
           }
-#pragma unroll 2
+#pragma unroll 4
           for (; rt < rtn; rt += 2) {
             const double2 vv = *reinterpret_cast<const double2*>(vcol + 8 * rt);
             const double2 av = *reinterpret_cast<const double2*>(acol + 8 * rt);
             dmma884(c0a, c1a, vv.x, av.x);
             dmma884(c0b, c1b, vv.y, av.y);
           }
-          *reinterpret_cast<double2*>(Wp + (size_t)(8 * ks + lq) * cpad + 8 * ct + 2 * lr) =
+          *reinterpret_cast<double2*>(Wp + (8 * ks + lq) * cpad + 8 * (j + ti) + 2 * lr) =
               make_double2(c0a + c0b, c1a + c1b);
         }
       }
@@ -351,59 +489,163 @@ k_lsq_wy(LsqArgs<double> a, const double* __restrict__ Mg, int ld, int cpad) {
       // S2: Z_i = tau_i (W_i - sum_{l<i} (v_i . v_l) Z_l), stored negated
       if (tid < 8 * ntrail) {
         const int col = 8 * (j + 1) + tid;
-        const double* g0 = Wp + 8 * j;
-        const double* g1 = Wp + (size_t)8 * cpad + 8 * j;
+        const double* b0 = Wp + 8 * j;
+        const double* b1 = b0 + 8 * cpad;
+        double gg[28], wv[8], tt[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          wv[i] = Wp[i * cpad + col] + Wp[(8 + i) * cpad + col];
+          tt[i] = tau_s[8 * j + i];
+#pragma unroll
+          for (int l = 0; l < i; ++l) gg[i * (i - 1) / 2 + l] = b0[i * cpad + l] + b1[i * cpad + l];
+        }
         double z[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          double wv = Wp[(size_t)i * cpad + col] + Wp[(size_t)(8 + i) * cpad + col];
+          double x = wv[i];
 #pragma unroll
-          for (int l = 0; l < i; ++l) wv = fma(-(g0[(size_t)i * cpad + l] + g1[(size_t)i * cpad + l]), z[l], wv);
-          z[i] = tau_s[8 * j + i] * wv;
-          Zs[(size_t)i * cpad + col] = -z[i];
-        }
-      }
-      __syncthreads();
-      // S3: A_trail -= V Z as A^T += (-Z)^T V^T, every warp its 8-row tiles
-      {
-        double za[NTM][2];
-#pragma unroll
-        for (int ti = 0; ti < NTM; ++ti) {
-          const bool ok = ti < ntrail;
-          const int cc = 8 * (j + 1 + ti) + lq;
-          za[ti][0] = ok ? Zs[(size_t)lr * cpad + cc] : 0.0;
-          za[ti][1] = ok ? Zs[(size_t)(lr + 4) * cpad + cc] : 0.0;
-        }
-        const double* v0 = A + (size_t)(8 * j + lr) * ld + lq;
-        const double* v1 = A + (size_t)(8 * j + lr + 4) * ld + lq;
-        for (int rt = j + warp; rt < rtn; rt += W) {
-          double b0 = v0[8 * rt], b1 = v1[8 * rt];
-          if (rt == j) {
-            b0 = (lq >= lr) ? b0 : 0.0;
-            b1 = (lq >= lr + 4) ? b1 : 0.0;
-          }
-          double* cbase = A + (size_t)(8 * (j + 1) + lq) * ld + 8 * rt + 2 * lr;
-#pragma unroll
-          for (int ti = 0; ti < NTM; ++ti) {
-            if (ti < ntrail) {
-              double2* cp = reinterpret_cast<double2*>(cbase + (size_t)8 * ti * ld);
-              double2 c = *cp;
-              dmma884(c.x, c.y, za[ti][0], b0);
-              dmma884(c.x, c.y, za[ti][1], b1);
-              *cp = c;
-            }
-          }
+          for (int l = 0; l < i; ++l) x = fma(-gg[i * (i - 1) / 2 + l], z[l], x);
+          z[i] = tt[i] * x;
+          Zs[i * cpad + col] = -z[i];
         }
       }
       __syncthreads();
       WY_PROF_MARK(4);
+      if (j + 1 < npanel) {
+        // the next panel's column tile first, then look-ahead
+        wy_s3<1>(A, Zs, ld, cpad, rtn, j, 0, 1, warp, W, lq, lr);
+        __syncthreads();
+        WY_PROF_MARK(5);
+        if (warp < kWyPanelWarps) wy_panel<RA>(A, ld, s, r, j + 1, warp, lane, tau_s, rdiag, nrm_s);
+        else wy_s3<NTM>(A, Zs, ld, cpad, rtn, j, 1, ntrail - 1, warp - kWyPanelWarps, W - kWyPanelWarps, lq, lr);
+        __syncthreads();
+        WY_PROF_MARK(2);
+      } else {
+        wy_s3<NTM>(A, Zs, ld, cpad, rtn, j, 0, ntrail, warp, W, lq, lr);
+        __syncthreads();
+        WY_PROF_MARK(5);
+      }
     }
-    sm_finish<double>(a, p, A, ld, mg, cvec, rdiag, nrm_s, rinfo, red, ld);
-    WY_PROF_MARK(5);
+
+    // rank test (linalg.py:107-112) and back substitution by warp 0
+    if (warp == 0) {
+      double mx = 0.0, mn = DBL_MAX;
+      int am = 0x7fffffff;
+      for (int jj = lane; jj < r; jj += 32) {
+        const double d = nrm_s[jj];
+        mx = fmax(mx, d);
+        if (d < mn) { mn = d; am = jj; }
+      }
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        const double pm = __shfl_xor_sync(0xffffffffu, mn, off);
+        const int pa = __shfl_xor_sync(0xffffffffu, am, off);
+        if (pm < mn || (pm == mn && pa < am)) { mn = pm; am = pa; }
+      }
+      const bool rankdef = r > 0 && mn < 1e-12 * fmax(mx, DBL_MIN);
+      if (lane == 0) {
+        rinfo[0] = rankdef ? 1.0 : 0.0;
+        rinfo[1] = (double)(am == 0x7fffffff ? 0 : am);
+      }
+      if (!rankdef) {
+        // column sweep: lane i holds y_i and y_{i+32}; R column k is contiguous and
+        // is fetched ahead of the dependent chain
+        const double rinv0 = (lane < r) ? 1.0 / rdiag[lane] : 0.0;
+        const double rinv1 = (lane + 32 < r) ? 1.0 / rdiag[lane + 32] : 0.0;
+        double y0 = (lane < r) ? A[r * ld + lane] : 0.0;
+        double y1 = (lane + 32 < r) ? A[r * ld + lane + 32] : 0.0;
+        int k = r - 1;
+        for (; k >= 32; --k) {          // pivots in the upper lane slot
+          const double r0 = A[k * ld + lane], r1 = A[k * ld + lane + 32];
+          const double ck = __shfl_sync(0xffffffffu, y1 * rinv1, k - 32);
+          if (lane == 0) cvec[k] = ck;
+          y0 = fma(-r0, ck, y0);
+          if (lane + 32 < k) y1 = fma(-r1, ck, y1);
+        }
+#pragma unroll 4
+        for (; k >= 0; --k) {
+          const double r0 = A[k * ld + lane];
+          const double ck = __shfl_sync(0xffffffffu, y0 * rinv0, k);
+          if (lane == 0) cvec[k] = ck;
+          if (lane < k) y0 = fma(-r0, ck, y0);
+        }
+      } else {
+        for (int jj = lane; jj < r; jj += 32) cvec[jj] = qnan;
+      }
+    }
+    __syncthreads();
+    WY_PROF_MARK(6);
+    const bool rankdef = rinfo[0] != 0.0;
+    // sampled residual ||w (M c - t)|| from the unweighted block in global memory
+    // (online.py:121-124): warp = columns warp + W q (t is column r with coefficient
+    // -1), lane = row pairs, four columns' loads in flight; per-warp row partials
+    // summed in warp order
+    {
+      double2 acc[4];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) acc[m] = make_double2(0.0, 0.0);
+      for (int jb = warp; jb <= r; jb += 4 * W) {
+        double2 mv[4][4];
+        double cj[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int jc = jb + q * W;
+          cj[q] = (jc < r) ? cvec[jc] : (jc == r ? -1.0 : 0.0);
+          const double2* col = reinterpret_cast<const double2*>(mg + (jc <= r ? jc : r) * ld);
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+            mv[q][m] = (lane + 32 * m < n2) ? __ldg(col + lane + 32 * m) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            acc[m].x = fma(mv[q][m].x, cj[q], acc[m].x);
+            acc[m].y = fma(mv[q][m].y, cj[q], acc[m].y);
+          }
+        }
+      }
+      double2* rb = reinterpret_cast<double2*>(A + warp * ld);
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        if (lane + 32 * m < n2) rb[lane + 32 * m] = acc[m];
+    }
+    for (int jj = tid; jj < r; jj += 32 * W) a.coef[p * r + jj] = cvec[jj];
+    __syncthreads();
+    double ss = 0.0;
+    for (int i = tid; i < s; i += 32 * W) {
+      double tot = A[i];
+#pragma unroll
+      for (int w = 1; w < W; ++w) tot += A[w * ld + i];
+      tot *= ws[i];
+      ss += tot * tot;
+    }
+    ss = warp_allreduce_d(ss);
+    if (lane == 0) red[warp] = ss;
+    __syncthreads();
+    issue_next();
+    if (tid == 0) {
+      double tot = 0.0;
+      for (int w = 0; w < W; ++w) tot += red[w];
+      a.sres[p] = rankdef ? qnan : sqrt(tot);
+      a.status[p] = rankdef ? 1 : 0;
+      if (a.badcol) a.badcol[p] = rankdef ? (int)rinfo[1] : -1;
+      if (a.outv) {
+        double o = 0.0;
+        if (a.proj)
+          for (int jj = 0; jj < r; ++jj) o += a.proj[jj] * cvec[jj];
+        a.outv[2 * p] = o;
+        a.outv[2 * p + 1] = 0.0;
+      }
+    }
+    __syncthreads();
+    WY_PROF_MARK(7);
   }
 #ifdef SAS_WY_PROF
   if (tid == 0 && blockIdx.x < 2)
-    printf("wy_prof block %d: load %lld weights %lld panel %lld S1 %lld S2+S3 %lld finish %lld cycles (all p of the CTA)\n",
-           blockIdx.x, wy_tp[0], wy_tp[1], wy_tp[2], wy_tp[3], wy_tp[4], wy_tp[5]);
+    printf("wy_prof block %d: load %lld weights %lld panel(+lookahead S3) %lld S1 %lld S2 %lld S3 %lld backsub %lld "
+           "residual %lld cycles (all p of the CTA)\n",
+           blockIdx.x, wy_tp[0], wy_tp[1], wy_tp[2], wy_tp[3], wy_tp[4], wy_tp[5], wy_tp[6], wy_tp[7]);
 #endif
 }

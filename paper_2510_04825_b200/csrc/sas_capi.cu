@@ -834,12 +834,13 @@ static int lsq_wy_env() {
   }
   return v;
 }
-template <int RA, int W, int MINB, int NTM>
+template <int RA, int MINB, int NTM>
 static int launch_lsq_wy_t(sas_plan* pl, const LsqArgs<double>& a, const double* mg, int ld, int cpad,
                            cudaStream_t st) {
   const size_t smem = lsq_wy_smem_bytes(ld, cpad);
-  auto kern = k_lsq_wy<RA, W, MINB, NTM>;
-  SMEM_OPTIN(k_lsq_wy<RA, W, MINB, NTM>);
+  constexpr int W = kWyWarps;
+  auto kern = k_lsq_wy<RA, MINB, NTM>;
+  SMEM_OPTIN(k_lsq_wy<RA, MINB, NTM>);
   int occ = 0;
   SAS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * W, smem));
   if (occ < 1) {
@@ -862,6 +863,7 @@ static int try_lsq_wy_stencil(sas_plan* pl, const LsqArgs<double>& a, const AsmS
   if (lsq_wy_env() < 0 && (lsq_sm_env() == 1 || lsq_cw_env() >= 0)) return -1;  // another kernel was asked for
   const int cols = a.r + 1, s = a.s;
   if (cols < (lsq_wy_env() == 1 ? 9 : 33) || cols > 56 || s > 224 || s < a.r || as.E + 1 > 8) return -1;
+  if (kWyWarps * wy_ld(s) > wy_ld(s) * wy_cpad(a.r)) return -1;   // residual partials reuse the matrix buffer
   const int ld = wy_ld(s), cpad = wy_cpad(a.r);
   const int64_t blk = (int64_t)ld * cpad * (int64_t)sizeof(double);
   int64_t chunk = (3ll << 29) / blk;
@@ -889,8 +891,8 @@ static int try_lsq_wy_stencil(sas_plan* pl, const LsqArgs<double>& a, const AsmS
     b.outv = a.outv ? a.outv + 2 * p0 : nullptr;
     b.status = a.status + p0;
     b.badcol = a.badcol ? a.badcol + p0 : nullptr;
-    if (s <= 160) rc = launch_lsq_wy_t<5, 8, 2, 6>(pl, b, pl->wy_mg, ld, cpad, st);
-    else rc = launch_lsq_wy_t<7, 8, 2, 6>(pl, b, pl->wy_mg, ld, cpad, st);
+    if (s <= 160) rc = launch_lsq_wy_t<5, 3, 6>(pl, b, pl->wy_mg, ld, cpad, st);
+    else rc = launch_lsq_wy_t<7, 2, 6>(pl, b, pl->wy_mg, ld, cpad, st);
     if (rc) return rc;
   }
   return SAS_OK;
