@@ -66,6 +66,18 @@ PEAK_SOURCE = ("measured FP64 microbenchmarks on this pool (profiles/r01_fp64_pe
 REF_DIR = ROOT / "baseline" / "_ref"
 
 
+def _hbm_peak_gbs() -> float:
+    """Measured copy bandwidth of this pool (driver-written MEASURED_PEAKS.json),
+    else the profiling recipe's fallback."""
+    try:
+        return float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+    except Exception:
+        return 6553.0
+
+
+HBM_PEAK_GBS = _hbm_peak_gbs()
+
+
 # --------------------------------------------------------------------------
 # algorithmic work per parameter value (SURVEY.md §8(d))
 # --------------------------------------------------------------------------
@@ -529,8 +541,11 @@ def main():
         return (sum(v) / len(v) if v else 0.0), len(v) / K, sum(v)
     k3_ms, k3_per_step, k3_sum = stage(_capi.SAS_STAGE_GAUSS_ROWS)
     k4_ms, k4_per_step, k4_sum = stage(_capi.SAS_STAGE_LSQ)
+    k2_ms, k2_per_step, k2_sum = stage(_capi.SAS_STAGE_STENCIL_ROWS)
     asm = assembly_flops(plan)
-    k4_flops_p = asm + lsq_flops(s, r, g.complex)
+    # the compact-WY path assembles the stencil rows in its own launches (K2); every
+    # other path fuses the assembly into K4
+    k4_flops_p = lsq_flops(s, r, g.complex) + (0.0 if k2_per_step else asm)
     stages = {"K4_lsq": {"ms_per_launch": round(k4_ms, 4), "launches_per_step": k4_per_step,
                          "share_of_step": round(k4_sum / max(local_ms, 1e-9), 4),
                          "flops_per_p": k4_flops_p,
@@ -538,6 +553,21 @@ def main():
                          if k4_ms else None}}
     stages["K4_lsq"]["frac_dfma_peak"] = (round(stages["K4_lsq"]["tflops"] / FP64_DFMA_PEAK_TFLOPS, 4)
                                           if stages["K4_lsq"]["tflops"] else None)
+    if k2_per_step:
+        ld = (s + 7) // 8 * 8
+        while ld % 16 != 8:
+            ld += 8
+        blk_bytes = ld * ((r + 1 + 7) // 8 * 8) * 8   # [M | t] block written per parameter value (HBM)
+        k2_gbs = blk_bytes * Pl / k2_per_step / (k2_ms / 1e3) / 1e9
+        stages["K2_stencil_rows"] = {"ms_per_launch": round(k2_ms, 4), "launches_per_step": k2_per_step,
+                                     "share_of_step": round(k2_sum / max(local_ms, 1e-9), 4),
+                                     "flops_per_p": asm, "bytes_written_per_p": blk_bytes,
+                                     "write_gbs": round(k2_gbs, 1),
+                                     "frac_hbm_peak": round(k2_gbs / HBM_PEAK_GBS, 4)}
+        both = (k2_sum + k4_sum) / K
+        stages["K4_lsq"]["tflops_with_assembly"] = round((asm + k4_flops_p) * Pl / (both / 1e3) / 1e12, 3)
+        stages["K4_lsq"]["frac_dfma_peak_with_assembly"] = round(
+            stages["K4_lsq"]["tflops_with_assembly"] / FP64_DFMA_PEAK_TFLOPS, 4)
     if k3_per_step:
         k3_flops_p = 2.0 * s * n * r
         k3_tf = k3_flops_p * Pl / k3_per_step / (k3_ms / 1e3) / 1e12
@@ -556,8 +586,11 @@ def main():
     else:
         st = stages["K4_lsq"]
         roofline = {"bound": "fp64", "pipe": "FP64 DFMA",
-                    "kernel": "K4 batched Householder least squares with the fused row assembly (k_lsq_*; CUDA "
-                              "events on the launching stream)", "achieved": st["tflops"],
+                    "kernel": ("K4 batched Householder least squares, compact-WY on DMMA (k_lsq_wy; the stencil rows "
+                               "are assembled by k_wy_stencil_rows, see stages; CUDA events on the launching stream)"
+                               if k2_per_step else
+                               "K4 batched Householder least squares with the fused row assembly (k_lsq_*; CUDA "
+                               "events on the launching stream)"), "achieved": st["tflops"],
                     "peak": FP64_DFMA_PEAK_TFLOPS, "frac": st["frac_dfma_peak"],
                     "traffic": ncu_traffic(f"k_lsq@cfg{cfg}"), "algorithmic_flops_per_p": st["flops_per_p"],
                     "launch_ms": st["ms_per_launch"], "share_of_step": st["share_of_step"]}

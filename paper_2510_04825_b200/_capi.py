@@ -32,7 +32,7 @@ EXPORTS = (
     "sas_plan_destroy", "sas_last_error", "sas_version", "sas_plan_set_timing", "sas_stage_times",
     "sas_tsqr_r", "sas_cg_stencil",
 )
-SAS_STAGE_LSQ, SAS_STAGE_GAUSS_ROWS = 1, 2
+SAS_STAGE_LSQ, SAS_STAGE_GAUSS_ROWS, SAS_STAGE_STENCIL_ROWS = 1, 2, 3
 #: test-only symbols (include/sas_debug.h)
 DEBUG_EXPORTS = ("sas_debug_exp64_host", "sas_debug_exp64")
 

@@ -862,7 +862,7 @@ static int try_lsq_wy_stencil(sas_plan* pl, const LsqArgs<double>& a, const AsmS
   if (lsq_wy_env() == 0 || lsq_force_cta()) return -1;
   if (lsq_wy_env() < 0 && (lsq_sm_env() == 1 || lsq_cw_env() >= 0)) return -1;  // another kernel was asked for
   const int cols = a.r + 1, s = a.s;
-  if (cols < (lsq_wy_env() == 1 ? 9 : 33) || cols > 56 || s > 224 || s < a.r || as.E + 1 > 8) return -1;
+  if (cols < (lsq_wy_env() == 1 ? 9 : 33) || cols > 56 || s > 224 || s < a.r || as.E + 1 > 8 || as.dp > 8) return -1;
   if (kWyWarps * wy_ld(s) > wy_ld(s) * wy_cpad(a.r)) return -1;   // residual partials reuse the matrix buffer
   const int ld = wy_ld(s), cpad = wy_cpad(a.r);
   const int64_t blk = (int64_t)ld * cpad * (int64_t)sizeof(double);
@@ -873,7 +873,7 @@ static int try_lsq_wy_stencil(sas_plan* pl, const LsqArgs<double>& a, const AsmS
   if (chunk > 65535ll * kWyPB) chunk = 65535ll * kWyPB;
   int rc = ensure(&pl->wy_mg, &pl->wy_mg_n, chunk * blk);
   if (rc) return rc;
-  const size_t rsmem = wy_rows_smem_bytes(as.E + 1, a.r);
+  const size_t rsmem = wy_rows_smem_bytes(as.E + 1, a.r, as.dp);
   if (int rc2 = smem_optin<k_wy_stencil_rows>(false)) return rc2;
   for (int64_t p0 = 0; p0 < a.P; p0 += chunk) {
     const int64_t pc = (a.P - p0 < chunk) ? (a.P - p0) : chunk;
