@@ -466,8 +466,8 @@ def main():
         for _ in range(8):
             online.solve_device(plan, params_t, out, stream)
         torch.cuda.synchronize(dev)
-    clk = clocks.stop(busy if local_ms < 1000.0 else None)
     local_ms = sum(a.elapsed_time(b) for a, b in ev)
+    clk = clocks.stop(busy if local_ms < 1000.0 else None)
     total_ms = parallel.max_over_ranks(local_ms, env.local_rank)
     ms_per_step = total_ms / K
     value = P_all * K / (total_ms / 1e3)
