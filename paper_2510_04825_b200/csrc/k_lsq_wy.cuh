@@ -176,79 +176,62 @@ constexpr int kWyPanelWarps = 4;
 __host__ __device__ inline size_t lsq_wy_smem_bytes(int ld, int cpad) {
   // A (reused for the residual's per-warp row partials, kWyWarps x ld <= ld x cpad);
   // W partials (2 x 8 x cpad) + Z (8 x cpad); weights (ld); tau / R_kk / |R_kk| / c
-  // (cpad each), residual partials (8), rank info (2), panel scalars (4), mbarrier
-  return ((size_t)ld * cpad + 24 * (size_t)cpad + ld + 4 * (size_t)cpad + 8 + 2 + 4) * sizeof(double) + 16;
+  // (cpad each), residual partials (8), rank info (2), mbarrier
+  return ((size_t)ld * cpad + 24 * (size_t)cpad + ld + 4 * (size_t)cpad + 8 + 2) * sizeof(double) + 16;
 }
 
 __device__ __forceinline__ void wy_bar_panel() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
 
 // Panel j: unblocked Householder on columns [8j, 8j+8), column-parallel over the
-// four panel warps: warp g holds columns g and g+4 in registers.  The panel
-// warps hold the rows at and below the panel's first row only: lane l, slot u =
-// row 8j + l + 32u (rows above are finished R rows), so the pivot row of step
-// KK is lane KK, slot 0 at compile time.
-//
-// Step k: the owner of column k writes the raw column a (rows >= 8j) and the
-// pair (|a[k:]|^2, a_k) to shared memory; after ONE named barrier every panel
-// warp reads them, forms the reflector scalars itself (|x| = sqrt, beta, tau,
-// head = a_k - beta: the same instructions on the same inputs in every warp, so
-// the sqrt / reciprocal chain overlaps the loads and the warp reduction instead
-// of sitting between two barriers) and reflects its remaining columns with
-// v^T y = a^T y - beta y_k (v = a - beta e_k), one warp reduction per step.  The
-// owner of the next pivot column reduces q = |y_{k+1}[k:]|^2 together with its
-// dot product: the reflection preserves q, so the next norm below row k is
-// q - y_{k+1,k}^2 (as exact as a direct sum unless one reflection removes most
-// of the column; then it is summed directly).  The heads go onto the diagonal
-// (V in place, R_kk = beta in rdiag) at the end of the panel.  Reflector
-// columns are k < r; the remaining panel columns (t, zero padding) are only
-// updated.
+// four panel warps: warp g holds columns g and g+4 in registers (lane l: rows
+// l + 32u).  Step k: the owner of column k forms the reflector (|x| from the
+// norm carried over from the previous step) and writes the column - V in place,
+// head on the diagonal - and tau to shared memory; after ONE named barrier the
+// four warps read v and reflect their remaining columns, each with one warp
+// reduction.  The owner of the next pivot column reduces q = |y_{k+1}[k:]|^2
+// together with its dot product: the reflection preserves q, so the next norm
+// below row k is q - y_{k+1,k}^2 (as exact as a direct sum unless one
+// reflection removes most of the column; then it is summed directly).
+// Reflector columns are k < r; the remaining panel columns (t, zero padding)
+// are only updated.
 template <int RA, int KK>
-__device__ __forceinline__ void wy_panel_step(double (&y)[2][RA], double& ss, double (&vh)[2], double* A, int ld,
-                                              int k0, int r, int g, int lane, const bool (&inb)[RA], double* sc,
-                                              double* tau_s, double* rdiag, double* nrm_s) {
+__device__ __forceinline__ void wy_panel_step(double (&y)[2][RA], double& ss, double* A, int ld, int s, int k0, int r,
+                                              int g, int lane, const bool (&inb)[RA], double* tau_s, double* rdiag,
+                                              double* nrm_s) {
   constexpr int OWN = KK & 3, SL = KK >> 2;
   const int k = k0 + KK;
   if (k >= r) return;   // uniform over the panel warps
   double* colk = A + k * ld + k0 + lane;   // row k0 + lane + 32u at colk[32u]
-  double* sck = sc + 2 * (KK & 1);
   if (g == OWN) {
+    const double alpha = __shfl_sync(0xffffffffu, y[SL][0], KK);   // row k: lane KK, slot 0
+    const double nrm = sqrt(ss);
+    const double aa = fabs(alpha);
+    double beta = 0.0, tau = 0.0;
+    if (nrm != 0.0) {
+      beta = (aa == 0.0) ? -nrm : copysign(nrm, -alpha);   // -sign(x_k) |x|
+      tau = rcp_nr(fma(nrm, aa, ss));                      // 1 / (|x| (|x| + |x_k|)), |x|^2 = ss
+    }
+    const double vhead = alpha - beta;
+    if (lane == KK) y[SL][0] = vhead;   // R above (lanes < KK), head, v below
 #pragma unroll
     for (int u = 0; u < RA; ++u)
       if (inb[u]) colk[32 * u] = y[SL][u];
-    if (lane == KK) {
-      sck[0] = ss;
-      sck[1] = y[SL][0];
-    }
-  }
-  wy_bar_panel();
-  const bool act0 = g > KK, act1 = g + 4 > KK;
-  if (!act1 && g != OWN) return;   // both of this warp's columns are finished (act0 implies act1)
-  const double ssk = sck[0], alpha = sck[1];
-  const double nrm = sqrt(ssk);
-  const double aa = fabs(alpha);
-  double beta = 0.0, tau = 0.0;
-  if (nrm != 0.0) {
-    beta = (aa == 0.0) ? -nrm : copysign(nrm, -alpha);   // -sign(x_k) |x|
-    tau = rcp_nr(fma(nrm, aa, ssk));                     // 1 / (|x| (|x| + |x_k|)), |x|^2 = ss
-  }
-  const double vhead = alpha - beta;
-  if (g == OWN) {
-    vh[SL] = vhead;
     if (lane == 0) {
       tau_s[k] = tau;
       rdiag[k] = beta;
       nrm_s[k] = nrm;
     }
   }
+  wy_bar_panel();
   if constexpr (KK < 7) {
     constexpr int NOWN = (KK + 1) & 3, NSL = (KK + 1) >> 2;
-    if (!act1) return;
-    const bool nxt = g == NOWN;
+    const bool act0 = g > KK, act1 = g + 4 > KK, nxt = g == NOWN;
+    if (!act1) return;   // both of this warp's columns are finished (act0 implies act1)
+    const double tau = tau_s[k];
     double v[RA];
 #pragma unroll
     for (int u = 0; u < RA; ++u) v[u] = inb[u] ? colk[32 * u] : 0.0;
     if (lane < KK) v[0] = 0.0;   // rows k0 .. k-1 of column k are R entries
-    const double yk0 = __shfl_sync(0xffffffffu, y[0][0], KK), yk1 = __shfl_sync(0xffffffffu, y[1][0], KK);
     double d0 = 0.0, d1 = 0.0, q = 0.0;
 #pragma unroll
     for (int u = 0; u < RA; ++u) {
@@ -273,9 +256,7 @@ __device__ __forceinline__ void wy_panel_step(double (&y)[2][RA], double& ss, do
         d1 += __shfl_xor_sync(0xffffffffu, d1, off);
       }
     }
-    // v = a - beta e_k: v^T y = a^T y - beta y_k
-    const double w0 = act0 ? tau * fma(-beta, yk0, d0) : 0.0, w1 = tau * fma(-beta, yk1, d1);
-    if (lane == KK) v[0] = vhead;
+    const double w0 = act0 ? tau * d0 : 0.0, w1 = tau * d1;
 #pragma unroll
     for (int u = 0; u < RA; ++u) {
       y[0][u] = fma(-w0, v[u], y[0][u]);
@@ -296,9 +277,12 @@ __device__ __forceinline__ void wy_panel_step(double (&y)[2][RA], double& ss, do
   }
 }
 
+// The panel warps hold the rows at and below the panel's first row only:
+// lane l, slot u = row 8j + l + 32u (rows above are finished R rows), so the
+// pivot row of step KK is lane KK, slot 0 at compile time.
 template <int RA>
-__device__ __forceinline__ void wy_panel(double* A, int ld, int s, int r, int j, int g, int lane, double* sc,
-                                         double* tau_s, double* rdiag, double* nrm_s) {
+__device__ __forceinline__ void wy_panel(double* A, int ld, int s, int r, int j, int g, int lane, double* tau_s,
+                                         double* rdiag, double* nrm_s) {
   const int k0 = 8 * j;
   bool inb[RA];
 #pragma unroll
@@ -310,29 +294,25 @@ __device__ __forceinline__ void wy_panel(double* A, int ld, int s, int r, int j,
 #pragma unroll
     for (int u = 0; u < RA; ++u) y[c][u] = inb[u] ? col[32 * u] : 0.0;
   }
-  double ss = 0.0, vh[2] = {0.0, 0.0};
+  double ss = 0.0;
   if (g == 0) {
 #pragma unroll
     for (int u = 0; u < RA; ++u) ss = fma(y[0][u], y[0][u], ss);
     ss = warp_allreduce_d(ss);
   }
-  wy_panel_step<RA, 0>(y, ss, vh, A, ld, k0, r, g, lane, inb, sc, tau_s, rdiag, nrm_s);
-  wy_panel_step<RA, 1>(y, ss, vh, A, ld, k0, r, g, lane, inb, sc, tau_s, rdiag, nrm_s);
-  wy_panel_step<RA, 2>(y, ss, vh, A, ld, k0, r, g, lane, inb, sc, tau_s, rdiag, nrm_s);
-  wy_panel_step<RA, 3>(y, ss, vh, A, ld, k0, r, g, lane, inb, sc, tau_s, rdiag, nrm_s);
-  wy_panel_step<RA, 4>(y, ss, vh, A, ld, k0, r, g, lane, inb, sc, tau_s, rdiag, nrm_s);
-  wy_panel_step<RA, 5>(y, ss, vh, A, ld, k0, r, g, lane, inb, sc, tau_s, rdiag, nrm_s);
-  wy_panel_step<RA, 6>(y, ss, vh, A, ld, k0, r, g, lane, inb, sc, tau_s, rdiag, nrm_s);
-  wy_panel_step<RA, 7>(y, ss, vh, A, ld, k0, r, g, lane, inb, sc, tau_s, rdiag, nrm_s);
-  // heads of this warp's pivot columns onto the diagonal (every panel warp is past
-  // its last read of those columns: the CTA barrier follows); columns that were no
-  // pivots (t, padding: k >= r) go back updated, tau = 0 for them
+  wy_panel_step<RA, 0>(y, ss, A, ld, s, k0, r, g, lane, inb, tau_s, rdiag, nrm_s);
+  wy_panel_step<RA, 1>(y, ss, A, ld, s, k0, r, g, lane, inb, tau_s, rdiag, nrm_s);
+  wy_panel_step<RA, 2>(y, ss, A, ld, s, k0, r, g, lane, inb, tau_s, rdiag, nrm_s);
+  wy_panel_step<RA, 3>(y, ss, A, ld, s, k0, r, g, lane, inb, tau_s, rdiag, nrm_s);
+  wy_panel_step<RA, 4>(y, ss, A, ld, s, k0, r, g, lane, inb, tau_s, rdiag, nrm_s);
+  wy_panel_step<RA, 5>(y, ss, A, ld, s, k0, r, g, lane, inb, tau_s, rdiag, nrm_s);
+  wy_panel_step<RA, 6>(y, ss, A, ld, s, k0, r, g, lane, inb, tau_s, rdiag, nrm_s);
+  wy_panel_step<RA, 7>(y, ss, A, ld, s, k0, r, g, lane, inb, tau_s, rdiag, nrm_s);
+  // columns that were no pivots (t, padding: k >= r) go back updated; tau = 0 for them
 #pragma unroll
   for (int c = 0; c < 2; ++c) {
     const int kc = k0 + g + 4 * c;
-    if (kc < r) {
-      if (lane == 0) A[kc * ld + kc] = vh[c];
-    } else {
+    if (kc >= r) {
       double* col = A + kc * ld + k0 + lane;
 #pragma unroll
       for (int u = 0; u < RA; ++u)
@@ -407,8 +387,7 @@ k_lsq_wy(LsqArgs<double> a, const double* __restrict__ Mg, int ld, int cpad) {
   double* cvec = nrm_s + cpad;
   double* red = cvec + cpad;
   double* rinfo = red + 8;
-  double* sc = rinfo + 2;                    // (|a[k:]|^2, a_k) of the current pivot, double-buffered
-  uint64_t* bar = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(sc + 4) + 7) & ~(uintptr_t)7);
+  uint64_t* bar = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(rinfo + 2) + 7) & ~(uintptr_t)7);
   const unsigned bytes = (unsigned)((size_t)ld * cpad * sizeof(double));
   const int64_t blk = (int64_t)ld * cpad;
   const int npanel = (r + 7) >> 3;
@@ -484,7 +463,7 @@ k_lsq_wy(LsqArgs<double> a, const double* __restrict__ Mg, int ld, int cpad) {
       continue;
     }
     WY_PROF_MARK(1);
-    if (warp < kWyPanelWarps) wy_panel<RA>(A, ld, s, r, 0, warp, lane, sc, tau_s, rdiag, nrm_s);
+    if (warp < kWyPanelWarps) wy_panel<RA>(A, ld, s, r, 0, warp, lane, tau_s, rdiag, nrm_s);
     __syncthreads();
     WY_PROF_MARK(2);
 
@@ -554,7 +533,7 @@ k_lsq_wy(LsqArgs<double> a, const double* __restrict__ Mg, int ld, int cpad) {
         wy_s3<1>(A, Zs, ld, cpad, rtn, j, 0, 1, warp, W, lq, lr);
         __syncthreads();
         WY_PROF_MARK(5);
-        if (warp < kWyPanelWarps) wy_panel<RA>(A, ld, s, r, j + 1, warp, lane, sc, tau_s, rdiag, nrm_s);
+        if (warp < kWyPanelWarps) wy_panel<RA>(A, ld, s, r, j + 1, warp, lane, tau_s, rdiag, nrm_s);
         else wy_s3<NTM>(A, Zs, ld, cpad, rtn, j, 1, ntrail - 1, warp - kWyPanelWarps, W - kWyPanelWarps, lq, lr);
         __syncthreads();
         WY_PROF_MARK(2);

@@ -268,7 +268,7 @@ class GpuPlan:
     def set_timing(self, enable: bool):
         _capi.check(self.lib.sas_plan_set_timing(self.handle, 1 if enable else 0), "sas_plan_set_timing")
 
-    def stage_times(self, cap: int = 64):
+    def stage_times(self, cap: int = 4096):
         """[(stage_id, ms)] for every kernel of the last solve (needs set_timing(True))."""
         ms = (C.c_float * cap)()
         st = (C.c_int32 * cap)()
