@@ -359,6 +359,119 @@ __device__ __forceinline__ void wy_s3(double* A, const double* Zs, int ld, int c
   }
 }
 
+// K2 inside the factorisation kernel (FUSED): the stencil rows of the NEXT
+// parameter value are assembled by the warps that idle while the panel warps
+// factor (one slice of row pairs per panel window) into this CTA's second
+// global slot, which stays in L2; the block never makes the HBM round trip of
+// the two-kernel path.  One warp per pair of selected rows: lanes 0..E-1 and
+// 8..8+E-1 evaluate the edge coefficients of the two rows, every lane then
+// builds the eight slot coefficients from shuffles and owns column pairs
+// (2 lane + 64 m, +1) loaded as 16-byte vectors.  Arithmetic identical to
+// AsmStencil (k_lsq.cuh): the blocks are bitwise what the other paths produce.
+struct WyAsm {
+  int E, dp;
+  const double* phi;     // s x E x dp
+  const double* G;       // s x (E+1) x r
+  const int8_t* gmap;    // s x (E+1)
+  double hh;
+  const double* params;  // P x dp
+  const double* t;       // s or P x s
+  int64_t t_stride;
+};
+
+// Row pairs [m_lo, m_hi) of the block of parameter value p, by a group of nthr
+// threads (rank tr; whole warps) synchronised by sync():
+//   stage 1  edge coefficients c_e = exp(sum_k p_k phi_k) / hh, one (row, edge) per thread
+//   stage 2  the eight slot coefficients of every row (diagonal in edge order)
+//   stage 3  products, one warp per row pair, every lane column pairs (2 lane + 64 m, +1)
+//            loaded as 16-byte vectors, the slot coefficients broadcast from shared memory
+// cbuf: 16 doubles per row of the range (edge coefficients, then slot coefficients).
+template <bool TWO, class Sync>
+__device__ __forceinline__ void wy_asm_pairs(const WyAsm& as, int64_t p, int s, int r, int ld, double* dst, int m_lo,
+                                             int m_hi, int tr, int nthr, double* cbuf, Sync sync) {
+  const int E = as.E, E1 = E + 1, dp = as.dp;
+  const int row0 = 2 * m_lo, nrw = 2 * (m_hi - m_lo);
+  if (nrw <= 0) return;
+  const double* pp = as.params + p * dp;
+  double* ce = cbuf;
+  double* cq = cbuf + 8 * nrw;
+  for (int idx = tr; idx < nrw * E; idx += nthr) {
+    const int rl = idx / E, e = idx - rl * E, row = row0 + rl;
+    double c = 0.0;
+    if (row < s) {
+      const double* ph = as.phi + ((int64_t)row * E + e) * dp;
+      double arg = dmul_exact(pp[0], ph[0]);
+      for (int k = 1; k < dp; ++k) arg = dadd_exact(arg, dmul_exact(pp[k], ph[k]));
+      c = exp(arg) / as.hh;
+    }
+    ce[rl * 8 + e] = c;
+  }
+  sync();
+  for (int idx = tr; idx < nrw * 8; idx += nthr) {
+    const int rl = idx >> 3, q = idx & 7, row = row0 + rl;
+    const int slot = (q < E1 && row < s) ? as.gmap[row * E1 + q] : -1;
+    double d = 0.0;
+    for (int e = 0; e < E; ++e) d = dadd_exact(d, ce[rl * 8 + e]);
+    cq[idx] = (slot < 0) ? 0.0 : (slot == 0 ? d : -ce[rl * 8 + slot - 1]);
+  }
+  sync();
+  const int wi = tr >> 5, nw = nthr >> 5, lane = tr & 31;
+  for (int m = m_lo + wi; m < m_hi; m += nw) {
+    const int i0 = 2 * m, rl = i0 - row0;
+    for (int jb = 2 * lane; jb < r; jb += 64) {
+      double mres[2][2];
+      const double* gr = as.G + ((int64_t)i0 * E1) * r + jb;
+      if constexpr (TWO) {
+        double2 gv[2][8];
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            gv[t][q] = (q < E1 && i0 + t < s) ? __ldcg(reinterpret_cast<const double2*>(gr + (int64_t)(t * E1 + q) * r))
+                                              : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const double2* c2 = reinterpret_cast<const double2*>(cq + (rl + t) * 8);
+          double mx = 0.0, my = 0.0;
+#pragma unroll
+          for (int q2 = 0; q2 < 4; ++q2) {
+            const double2 c = c2[q2];
+            if (2 * q2 < E1) { mx = fma(c.x, gv[t][2 * q2].x, mx); my = fma(c.x, gv[t][2 * q2].y, my); }
+            if (2 * q2 + 1 < E1) { mx = fma(c.y, gv[t][2 * q2 + 1].x, mx); my = fma(c.y, gv[t][2 * q2 + 1].y, my); }
+          }
+          mres[t][0] = mx;
+          mres[t][1] = my;
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          double2 gv[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            gv[q] = (q < E1 && i0 + t < s) ? __ldcg(reinterpret_cast<const double2*>(gr + (int64_t)(t * E1 + q) * r))
+                                           : make_double2(0.0, 0.0);
+          const double2* c2 = reinterpret_cast<const double2*>(cq + (rl + t) * 8);
+          double mx = 0.0, my = 0.0;
+#pragma unroll
+          for (int q2 = 0; q2 < 4; ++q2) {
+            const double2 c = c2[q2];
+            if (2 * q2 < E1) { mx = fma(c.x, gv[2 * q2].x, mx); my = fma(c.x, gv[2 * q2].y, my); }
+            if (2 * q2 + 1 < E1) { mx = fma(c.y, gv[2 * q2 + 1].x, mx); my = fma(c.y, gv[2 * q2 + 1].y, my); }
+          }
+          mres[t][0] = mx;
+          mres[t][1] = my;
+        }
+      }
+      *reinterpret_cast<double2*>(dst + (int64_t)jb * ld + i0) = make_double2(mres[0][0], mres[1][0]);
+      *reinterpret_cast<double2*>(dst + (int64_t)(jb + 1) * ld + i0) = make_double2(mres[0][1], mres[1][1]);
+    }
+    if (lane < 2) dst[(int64_t)r * ld + i0 + lane] = (i0 + lane < s) ? as.t[p * as.t_stride + i0 + lane] : 0.0;
+  }
+}
+
+struct WySyncCta { __device__ __forceinline__ void operator()() const { __syncthreads(); } };
+struct WySyncUpd { __device__ __forceinline__ void operator()() const { asm volatile("bar.sync 2, 128;\n" ::: "memory"); } };
+
 #ifdef SAS_WY_PROF
 #define WY_PROF_MARK(ph) do { wy_t1 = clock64(); wy_tp[ph] += wy_t1 - wy_t0; wy_t0 = wy_t1; } while (0)
 #else
@@ -369,9 +482,10 @@ __device__ __forceinline__ void wy_s3(double* A, const double* Zs, int ld, int c
 // r + 1 <= 8 (NTM + 1) columns.  Mg: P blocks of ld x cpad doubles (k_wy_stencil_rows).
 // Per panel: S1 (all warps) | S2 | S3 on the next panel's column tile (all warps) |
 // warps 0..3 factor the next panel while warps 4..7 finish S3 (look-ahead).
-template <int RA, int MINB, int NTM>
+// FUSED: Mg holds two blocks per CTA (slots), filled by the CTA itself (wy_asm_pairs).
+template <int RA, int MINB, int NTM, bool FUSED>
 __global__ void __launch_bounds__(32 * kWyWarps, MINB)
-k_lsq_wy(LsqArgs<double> a, const double* __restrict__ Mg, int ld, int cpad) {
+k_lsq_wy(LsqArgs<double> a, double* __restrict__ Mg, int ld, int cpad, WyAsm as) {
   constexpr int W = kWyWarps;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -395,35 +509,58 @@ k_lsq_wy(LsqArgs<double> a, const double* __restrict__ Mg, int ld, int cpad) {
   const int n2 = ld >> 1;
   const double qnan = __longlong_as_double(0x7ff8000000000000ll);
   for (int i = tid; i < ld; i += 32 * W) ws[i] = (a.w && i < s) ? a.w[i] : 1.0;
+  const int s2 = (s + 1) >> 1;                               // row pairs
+  const int spw = (s2 + npanel - 1) / (npanel > 0 ? npanel : 1);   // row pairs per panel window
+  double* slots = Mg + (int64_t)blockIdx.x * 2 * blk;       // FUSED: this CTA's two blocks
   if (tid == 0) {
     mbar_init(bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    if ((int64_t)blockIdx.x < a.P) {
-      mbar_expect_tx(bar, bytes);
-      bulk_g2s(A, Mg + (int64_t)blockIdx.x * blk, bytes, bar);
+  }
+  if (FUSED && (int64_t)blockIdx.x < a.P) {
+    // first block of this CTA, by all warps, in slices that fit the coefficient scratch
+    for (int lo = 0; lo < s2; lo += spw) {
+      wy_asm_pairs<MINB <= 2>(as, blockIdx.x, s, r, ld, slots, lo, lo + spw < s2 ? lo + spw : s2, tid, 32 * W, Wp,
+                              WySyncCta{});
+      __syncthreads();
     }
   }
   __syncthreads();
+  if (tid == 0 && (int64_t)blockIdx.x < a.P) {
+    asm volatile("fence.proxy.async;\n" ::: "memory");
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(A, FUSED ? slots : Mg + (int64_t)blockIdx.x * blk, bytes, bar);
+  }
   unsigned phase = 0;
+  int it = 0;
 #ifdef SAS_WY_PROF
   long long wy_tp[8] = {0, 0, 0, 0, 0, 0, 0, 0}, wy_t0 = clock64(), wy_t1;
 #endif
 
-  for (int64_t p = blockIdx.x; p < a.P; p += gridDim.x) {
-    const double* mg = Mg + p * blk;
+  for (int64_t p = blockIdx.x; p < a.P; p += gridDim.x, ++it) {
+    const double* mg = FUSED ? slots + (it & 1) * blk : Mg + p * blk;
+    double* mg_next = slots + ((it + 1) & 1) * blk;
+    const bool has_next = p + gridDim.x < a.P;
     // the next parameter value's block: issued as soon as A is dead (after the
     // residual's row partials, which reuse A, are summed; all generic-proxy accesses to
-    // A are ordered before the async-proxy write by the preceding barrier and the
-    // proxy fence)
+    // A - and, FUSED, this CTA's global stores of the block - are ordered before the
+    // async-proxy copy by the preceding barrier and the proxy fence)
     auto issue_next = [&]() {
-      if (tid == 0 && p + gridDim.x < a.P) {
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      if (tid == 0 && has_next) {
+        asm volatile("fence.proxy.async;\n" ::: "memory");
         mbar_expect_tx(bar, bytes);
-        bulk_g2s(A, mg + (int64_t)gridDim.x * blk, bytes, bar);
-        if (p + 2 * (int64_t)gridDim.x < a.P)
+        bulk_g2s(A, FUSED ? mg_next : mg + (int64_t)gridDim.x * blk, bytes, bar);
+        if (!FUSED && p + 2 * (int64_t)gridDim.x < a.P)
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(mg + 2 * (int64_t)gridDim.x * blk),
                        "r"(bytes)
                        : "memory");
+      }
+    };
+    // FUSED: window w of the panel schedule assembles row pairs [w spw, (w+1) spw) of the next block
+    auto asm_window = [&](int w) {
+      if (FUSED && has_next) {
+        const int lo = w * spw, hi = (lo + spw < s2) ? lo + spw : s2;
+        wy_asm_pairs<MINB <= 2>(as, p + gridDim.x, s, r, ld, mg_next, lo, hi, tid - 32 * kWyPanelWarps,
+                                32 * (W - kWyPanelWarps), Wp, WySyncUpd{});
       }
     };
     mbar_wait(bar, phase);
@@ -459,11 +596,19 @@ k_lsq_wy(LsqArgs<double> a, const double* __restrict__ Mg, int ld, int cpad) {
     }
     if (__syncthreads_or(bad)) {
       lsq_nonfinite<double>(a, p);
+      if (FUSED && has_next) {   // no panel windows for this parameter value: assemble the next block now
+        for (int lo = 0; lo < s2; lo += spw) {
+          wy_asm_pairs<MINB <= 2>(as, p + gridDim.x, s, r, ld, mg_next, lo, lo + spw < s2 ? lo + spw : s2, tid, 32 * W,
+                                  Wp, WySyncCta{});
+          __syncthreads();
+        }
+      }
       issue_next();
       continue;
     }
     WY_PROF_MARK(1);
     if (warp < kWyPanelWarps) wy_panel<RA>(A, ld, s, r, 0, warp, lane, tau_s, rdiag, nrm_s);
+    else asm_window(0);
     __syncthreads();
     WY_PROF_MARK(2);
 
@@ -534,7 +679,10 @@ k_lsq_wy(LsqArgs<double> a, const double* __restrict__ Mg, int ld, int cpad) {
         __syncthreads();
         WY_PROF_MARK(5);
         if (warp < kWyPanelWarps) wy_panel<RA>(A, ld, s, r, j + 1, warp, lane, tau_s, rdiag, nrm_s);
-        else wy_s3<NTM>(A, Zs, ld, cpad, rtn, j, 1, ntrail - 1, warp - kWyPanelWarps, W - kWyPanelWarps, lq, lr);
+        else {
+          wy_s3<NTM>(A, Zs, ld, cpad, rtn, j, 1, ntrail - 1, warp - kWyPanelWarps, W - kWyPanelWarps, lq, lr);
+          asm_window(j + 1);
+        }
         __syncthreads();
         WY_PROF_MARK(2);
       } else {
@@ -612,7 +760,7 @@ k_lsq_wy(LsqArgs<double> a, const double* __restrict__ Mg, int ld, int cpad) {
           const double2* col = reinterpret_cast<const double2*>(mg + (jc <= r ? jc : r) * ld);
 #pragma unroll
           for (int m = 0; m < 4; ++m)
-            mv[q][m] = (lane + 32 * m < n2) ? __ldg(col + lane + 32 * m) : make_double2(0.0, 0.0);
+            mv[q][m] = (lane + 32 * m < n2) ? __ldcg(col + lane + 32 * m) : make_double2(0.0, 0.0);
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {

@@ -174,6 +174,8 @@ struct sas_plan {
   int64_t cw_mg_n = 0;
   double* wy_mg = nullptr;   // K4 compact-WY kernel: [M | t] blocks of a parameter chunk (k_wy_stencil_rows)
   int64_t wy_mg_n = 0;
+  double* wy_slots = nullptr;  // fused K2: two [M | t] blocks per resident CTA (zero padding set at allocation)
+  int64_t wy_slots_n = 0;
   int64_t Mscr_P = 0;
   double* rpart = nullptr;
   int64_t rpart_n = 0;
@@ -292,7 +294,7 @@ static void plan_free(sas_plan* pl) {
   DevGuard g(pl->device);
   void* ptrs[] = {pl->X, pl->S, pl->w, pl->t, pl->proj, pl->kind, pl->scale, pl->rate, pl->blocks,
                   pl->phi, pl->G, pl->gmap, pl->pts, pl->D, pl->Dfrag, pl->Xfrag, pl->full_nbr, pl->full_phi, pl->full_b,
-                  pl->csr_rp_d, pl->csr_ci_d, pl->csr_va_d, pl->Mscr, pl->cw_mg, pl->wy_mg, pl->rpart, pl->xscr, pl->fco,
+                  pl->csr_rp_d, pl->csr_ci_d, pl->csr_va_d, pl->Mscr, pl->cw_mg, pl->wy_mg, pl->wy_slots, pl->rpart, pl->xscr, pl->fco,
                   pl->h_params, pl->h_ctab, pl->h_rhs, pl->h_coef, pl->h_sres, pl->h_outv,
                   pl->h_status, pl->h_bad};
   for (void* p : ptrs)
@@ -834,13 +836,13 @@ static int lsq_wy_env() {
   }
   return v;
 }
-template <int RA, int MINB, int NTM>
-static int launch_lsq_wy_t(sas_plan* pl, const LsqArgs<double>& a, const double* mg, int ld, int cpad,
+template <int RA, int MINB, int NTM, bool FUSED>
+static int launch_lsq_wy_t(sas_plan* pl, const LsqArgs<double>& a, double* mg, int ld, int cpad, const WyAsm& wa,
                            cudaStream_t st) {
-  const size_t smem = lsq_wy_smem_bytes(ld, cpad);
   constexpr int W = kWyWarps;
-  auto kern = k_lsq_wy<RA, MINB, NTM>;
-  SMEM_OPTIN(k_lsq_wy<RA, MINB, NTM>);
+  const size_t smem = lsq_wy_smem_bytes(ld, cpad);
+  auto kern = k_lsq_wy<RA, MINB, NTM, FUSED>;
+  SMEM_OPTIN(k_lsq_wy<RA, MINB, NTM, FUSED>);
   int occ = 0;
   SAS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * W, smem));
   if (occ < 1) {
@@ -848,14 +850,37 @@ static int launch_lsq_wy_t(sas_plan* pl, const LsqArgs<double>& a, const double*
     return SAS_ERR_ARG;
   }
   int64_t grid = (int64_t)occ * pl->sms;
+  if (FUSED) {
+    // two [M | t] blocks per resident CTA (L2-resident), zero padding set once
+    const int64_t need = grid * 2 * (int64_t)ld * cpad * (int64_t)sizeof(double);
+    if (pl->wy_slots_n < need || !pl->wy_slots) {
+      const int rc = ensure(&pl->wy_slots, &pl->wy_slots_n, need);
+      if (rc) return rc;
+      SAS_CUDA_CHECK(cudaMemsetAsync(pl->wy_slots, 0, (size_t)need, st));
+    }
+    mg = pl->wy_slots;
+  }
   if (grid > a.P) grid = a.P;
   if (grid < 1) grid = 1;
   stage_begin(pl, st, SAS_STAGE_LSQ);
-  kern<<<(unsigned)grid, 32 * W, smem, st>>>(a, mg, ld, cpad);
+  kern<<<(unsigned)grid, 32 * W, smem, st>>>(a, mg, ld, cpad, wa);
   stage_end(pl, st);
   SAS_CUDA_CHECK(cudaGetLastError());
   pl->last_launches++;
   return SAS_OK;
+}
+// SAS_LSQ_WY_FUSED=1: K2 inside k_lsq_wy (the idle warps of each panel window assemble
+// the next block into the CTA's L2 slots; no HBM round trip, one launch per sweep).
+// Measured slower than the default two-kernel path (config 5: 36.4 vs 27.0 ms, config 3:
+// 12.7 vs 9.2 ms): four warps do not hide the L2 latency of the 560 KB of gathered rows
+// inside a panel window (profiles/r02_k4_wy_tuning.txt).
+static bool lsq_wy_fused() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SAS_LSQ_WY_FUSED");
+    v = (e && atoi(e)) ? 1 : 0;
+  }
+  return v == 1;
 }
 // returns -1 when the shape is not covered
 static int try_lsq_wy_stencil(sas_plan* pl, const LsqArgs<double>& a, const AsmStencil& as, cudaStream_t st) {
@@ -865,6 +890,13 @@ static int try_lsq_wy_stencil(sas_plan* pl, const LsqArgs<double>& a, const AsmS
   if (cols < (lsq_wy_env() == 1 ? 9 : 33) || cols > 56 || s > 224 || s < a.r || as.E + 1 > 8 || as.dp > 8) return -1;
   if (kWyWarps * wy_ld(s) > wy_ld(s) * wy_cpad(a.r)) return -1;   // residual partials reuse the matrix buffer
   const int ld = wy_ld(s), cpad = wy_cpad(a.r);
+  const WyAsm wa{as.E, as.dp, as.phi, as.G, as.gmap, as.hh, as.params, a.t, a.t_stride};
+  const int npan = (a.r + 7) / 8, spw = ((s + 1) / 2 + npan - 1) / npan;
+  if (lsq_wy_fused() && (a.r & 1) == 0 && 2 * spw <= cpad) {   // coefficient scratch: 16 doubles per row of a window
+    // K2 inside the kernel: the idle warps of each panel window assemble the next block
+    if (s <= 160) return launch_lsq_wy_t<5, 3, 6, true>(pl, a, nullptr, ld, cpad, wa, st);
+    return launch_lsq_wy_t<7, 2, 6, true>(pl, a, nullptr, ld, cpad, wa, st);
+  }
   const int64_t blk = (int64_t)ld * cpad * (int64_t)sizeof(double);
   int64_t chunk = (3ll << 29) / blk;
   if (const char* e = getenv("SAS_LSQ_WY_CHUNK")) chunk = atoll(e);
@@ -891,8 +923,8 @@ static int try_lsq_wy_stencil(sas_plan* pl, const LsqArgs<double>& a, const AsmS
     b.outv = a.outv ? a.outv + 2 * p0 : nullptr;
     b.status = a.status + p0;
     b.badcol = a.badcol ? a.badcol + p0 : nullptr;
-    if (s <= 160) rc = launch_lsq_wy_t<5, 3, 6>(pl, b, pl->wy_mg, ld, cpad, st);
-    else rc = launch_lsq_wy_t<7, 2, 6>(pl, b, pl->wy_mg, ld, cpad, st);
+    if (s <= 160) rc = launch_lsq_wy_t<5, 3, 6, false>(pl, b, pl->wy_mg, ld, cpad, wa, st);
+    else rc = launch_lsq_wy_t<7, 2, 6, false>(pl, b, pl->wy_mg, ld, cpad, wa, st);
     if (rc) return rc;
   }
   return SAS_OK;

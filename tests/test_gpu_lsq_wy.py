@@ -91,6 +91,32 @@ def test_wy_chunked_sweep_is_bitwise_batch_independent():
     out.unlink()
 
 
+def test_wy_fused_assembly_equals_two_kernel_path():
+    """The two-kernel path (k_wy_stencil_rows + k_lsq_wy per chunk, the default) and the
+    fused path (SAS_LSQ_WY_FUSED=1: the next block assembled by the idle warps into the
+    CTA's L2 slots) build bitwise the same blocks and run the same factorisation."""
+    prob, basis, sel = _case("3d", 10, 200, 50, seed=5)
+    plan = online.precompute_online(prob.system, basis, sel)
+    res = online.solve_params(plan, prob.test_params(1500))
+    env = dict(os.environ, SAS_LSQ_WY_FUSED="1")
+    code = ("import numpy as np, sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+            "from test_gpu_lsq_wy import _case; from paper_2510_04825_b200 import online\n"
+            "prob, basis, sel = _case('3d', 10, 200, 50, seed=5)\n"
+            "plan = online.precompute_online(prob.system, basis, sel)\n"
+            "res = online.solve_params(plan, prob.test_params(1500))\n"
+            "np.save(sys.argv[1], np.concatenate([res.coefficients, res.sampled_residual[:, None]], axis=1))\n"
+            ) % (str(ROOT), str(ROOT / "tests"))
+    out = ROOT / "gpurun_out" / "_wy_two.npy"
+    out.parent.mkdir(exist_ok=True)
+    r = subprocess.run([sys.executable, "-c", code, str(out)], cwd=ROOT, env=env, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    other = np.load(out)
+    out.unlink()
+    assert np.array_equal(other[:, :-1], res.coefficients)
+    assert np.array_equal(other[:, -1], res.sampled_residual)
+
+
 def test_wy_matches_column_owner_kernel():
     """Same reflectors, different blocking: the two kernels agree to rounding."""
     prob, basis, sel = _case("2d", 32, 160, 40, seed=11)
