@@ -88,23 +88,37 @@ k_wy_stencil_rows(int E, int dp, const double* __restrict__ phi, const double* _
   for (int idx = tid; idx < gcount; idx += 256) Gs[idx] = __ldg(gsrc + idx);
   for (int idx = tid; idx < np * dp; idx += 256) ps[idx] = __ldg(params + p0 * dp + idx);
   __syncthreads();
-  // edge coefficients: thread = (row, edge) pair x parameter values pl = tid/64, +4, ...;
-  // phi of the pair in registers, the parameter values broadcast from shared memory
+  // edge coefficients: thread = (row, edge) pair x parameter values pl = group, + groups, ...
+  // (groups = 256 / pairs); phi of the pair in registers, the parameter values broadcast
+  // from shared memory; four independent exp / division chains in flight per thread
   {
-    const int pair = tid & 63, pg = tid >> 6;
-    if (pair < nrows * E) {
+    const int npair = nrows * E;
+    const int groups = npair > 0 ? 256 / npair : 0;
+    const int pg = npair > 0 ? tid / npair : 0, pair = npair > 0 ? tid - pg * npair : 0;
+    if (pg < groups) {
       const int i = pair / E, e = pair - i * E;
       const double* ph = phi + ((int64_t)(i0 + i) * E + e) * dp;
       double phr[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) phr[k] = (k < dp) ? __ldg(ph + k) : 0.0;
-      for (int pl = pg; pl < np; pl += 4) {
-        const double* pp = ps + pl * dp;
-        double arg = dmul_exact(pp[0], phr[0]);
+      double* cdst = ce + i * 8 + e;
+      for (int pl = pg; pl < np; pl += 4 * groups) {
+        double arg[4];
 #pragma unroll
-        for (int k = 1; k < 8; ++k)
-          if (k < dp) arg = dadd_exact(arg, dmul_exact(pp[k], phr[k]));
-        ce[(pl * kWyRB + i) * 8 + e] = exp(arg) / hh;
+        for (int u = 0; u < 4; ++u) {
+          const int pu = pl + u * groups;
+          const double* pp = ps + (pu < np ? pu : pl) * dp;
+          arg[u] = dmul_exact(pp[0], phr[0]);
+#pragma unroll
+          for (int k = 1; k < 8; ++k)
+            if (k < dp) arg[u] = dadd_exact(arg[u], dmul_exact(pp[k], phr[k]));
+        }
+        double cv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) cv[u] = exp(arg[u]) / hh;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (pl + u * groups < np) cdst[(pl + u * groups) * kWyRB * 8] = cv[u];
       }
     }
   }
@@ -142,6 +156,7 @@ k_wy_stencil_rows(int E, int dp, const double* __restrict__ phi, const double* _
   const int64_t ostep = 2 * (int64_t)cpad * ld;
   const double2* c2 = reinterpret_cast<const double2*>(cs) + half * 4 * kWyRB + i;
   const double* tp = t + (p0 + half) * t_stride + row;
+#pragma unroll 2
   for (int pl = half; pl < np; pl += 2) {
     double m[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
