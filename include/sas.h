@@ -199,6 +199,19 @@ int32_t sas_stage_times(sas_plan* plan, float* ms, int32_t* stage, int32_t cap);
  * Stream-ordered; scratch comes from the stream-ordered allocator. */
 int sas_tsqr_r(const void* A, int64_t m, int32_t w, int32_t dtype, void* R, int32_t device, void* stream);
 
+/* Leverage-score row selection, dense part (replaces subsample._range_basis +
+ * leverage_scores, subsample.py:84-94, 144-159, for tall targets): Q = A C and
+ * scores_i = ||Q_i||^2.  The caller builds C from sas_tsqr_r's R factor (SVD of
+ * the small R on the host, then C <- C R2^-1 from the R factor of Q until Q is
+ * orthonormal to rounding: offline.leverage_scores_gpu).
+ *   A       m x w row-major, device, dtype SAS_F64 / SAS_C128
+ *   C       w x k row-major, HOST (k <= w <= 64)
+ *   Q       m x k row-major, device, or NULL
+ *   scores  m doubles, device, or NULL
+ * Stream-ordered; fixed summation order. */
+int sas_range_rows(const void* A, int64_t m, int32_t w, const void* C, int32_t k, int32_t dtype, void* Q,
+                   double* scores, int32_t device, void* stream);
+
 /* Offline snapshot solve of a stencil system (replaces full_solve,
  * systems.py:187-222, for configs 3 and 5): Jacobi-preconditioned CG on
  *   (A v)_i = dg_i v_i - sum_e ct[i][e] v_{nbr[i][e]}   (nbr = -1: Dirichlet edge)
@@ -215,6 +228,20 @@ int sas_cg_stencil(int64_t n, int32_t E, const double* dg, const double* ct, con
 void sas_plan_destroy(sas_plan* plan);
 const char* sas_last_error(void);
 const char* sas_version(void);
+
+/* Offline snapshot solve of a large affine system (replaces full_solve,
+ * systems.py:187-222, for config 4): Jacobi-preconditioned BiCGSTAB on the
+ * CSR matrix A(p) = sum_k f_k(p) A_k with fused kernels (k_bicg.cuh: direction
+ * update, SpMV with its dot products, vector updates; device-side fixed-order
+ * reductions).  Stops at ||r|| <= tol ||b|| or ||r|| <= 1e-12 (a_norm ||x|| +
+ * ||b||), checked every check_every iterations.
+ *   rowptr (n + 1), colind (nnz)  int32, device;  val (nnz), diag, b, x (n)  dtype, device
+ * Outputs: iterations, the TRUE residual ||b - A x|| and ||x|| (the caller
+ * applies the reference's residual guard). */
+int sas_bicgstab_csr(int64_t n, const int32_t* rowptr, const int32_t* colind, const void* val, const void* diag,
+                     const void* b, void* x, int32_t dtype, double tol, double a_norm, int32_t maxiter,
+                     int32_t check_every, int32_t device, void* stream, int32_t* iters_out, double* rnorm_out,
+                     double* xnorm_out);
 
 #ifdef __cplusplus
 }

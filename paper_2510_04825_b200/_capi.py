@@ -30,7 +30,7 @@ EXPORTS = (
     "sas_plan_create", "sas_solve", "sas_solve_host", "sas_lift", "sas_residual",
     "sas_plan_set_operator", "sas_plan_info", "sas_last_launch_count",
     "sas_plan_destroy", "sas_last_error", "sas_version", "sas_plan_set_timing", "sas_stage_times",
-    "sas_tsqr_r", "sas_cg_stencil",
+    "sas_tsqr_r", "sas_cg_stencil", "sas_range_rows", "sas_bicgstab_csr",
 )
 SAS_STAGE_LSQ, SAS_STAGE_GAUSS_ROWS, SAS_STAGE_STENCIL_ROWS = 1, 2, 3
 #: test-only symbols (include/sas_debug.h)
@@ -98,6 +98,11 @@ def _declare(lib):
     lib.sas_debug_exp64.restype = C.c_int
     lib.sas_tsqr_r.argtypes = [vp, i64, i32, i32, vp, i32, vp]
     lib.sas_tsqr_r.restype = C.c_int
+    lib.sas_range_rows.argtypes = [vp, i64, i32, vp, i32, i32, vp, vp, i32, vp]
+    lib.sas_range_rows.restype = C.c_int
+    lib.sas_bicgstab_csr.argtypes = [i64, vp, vp, vp, vp, vp, vp, i32, C.c_double, C.c_double, i32, i32, i32, vp,
+                                     C.POINTER(i32), dp, dp]
+    lib.sas_bicgstab_csr.restype = C.c_int
     lib.sas_cg_stencil.argtypes = [i64, i32, vp, vp, vp, vp, vp, C.c_double, C.c_double, i32, i32, i32, vp,
                                    C.POINTER(i32), dp, dp]
     lib.sas_cg_stencil.restype = C.c_int

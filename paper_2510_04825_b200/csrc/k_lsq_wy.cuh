@@ -58,7 +58,18 @@ __host__ __device__ inline int wy_cpad(int r) { return (r + 1 + 7) / 8 * 8; }
 // sum, exp()/hh, diagonal in edge order, FMA chain over the gathered rows in G
 // order - the blocks are bitwise what the fused assembler produces.
 constexpr int kWyRB = 8;
-constexpr int kWyPB = 32;
+#ifndef SAS_WY_PB
+#define SAS_WY_PB 32
+#endif
+#ifndef SAS_WY_CPT
+#define SAS_WY_CPT 4
+#endif
+constexpr int kWyPB = SAS_WY_PB;    // parameter values per CTA
+constexpr int kWyCPT = SAS_WY_CPT;  // columns per thread in the product phase (4: two p-halves of 128 threads; 2: one)
+static_assert(kWyPB <= 32 && (kWyCPT == 2 || kWyCPT == 4), "k_wy_stencil_rows: 256 threads = 32 parameter values x 8 rows in the slot phase");
+#ifndef SAS_WY_MINB
+#define SAS_WY_MINB 1
+#endif
 
 __host__ __device__ inline size_t wy_rows_smem_bytes(int E1, int r, int dp) {
   // gathered rows (RB x E1 x r), slot coefficients [p][q/2][row] (double2), edge
@@ -66,7 +77,7 @@ __host__ __device__ inline size_t wy_rows_smem_bytes(int E1, int r, int dp) {
   return (((size_t)kWyRB * E1 * r + 1) / 2 * 2 + 2 * (size_t)kWyPB * kWyRB * 8 + (size_t)kWyPB * dp) * sizeof(double);
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, SAS_WY_MINB)
 k_wy_stencil_rows(int E, int dp, const double* __restrict__ phi, const double* __restrict__ G,
                   const int8_t* __restrict__ gmap, double hh, const double* __restrict__ params,
                   const double* __restrict__ t, int64_t t_stride, int64_t P, int s, int r, int ld, int cpad,
@@ -140,47 +151,53 @@ k_wy_stencil_rows(int E, int dp, const double* __restrict__ phi, const double* _
     }
   }
   __syncthreads();
-  // products: thread = (row i, four columns), the gathered rows of its columns in
-  // registers for the parameter values pl = tid/128, +2, ...
-  const int i = tid & 7, j0 = 4 * ((tid >> 3) & 15), half = tid >> 7;
+  // products: thread = (row i, kWyCPT columns), the gathered rows of its columns in
+  // registers for the parameter values pl = half, half + NH, ...
+  constexpr int CPT = kWyCPT, NG = 64 / CPT, NH = 256 / (kWyRB * NG);
+  const int i = tid & 7, j0 = CPT * ((tid >> 3) % NG), half = tid / (kWyRB * NG);
   if (j0 >= cpad) return;
   const int row = i0 + i;
   const bool rok = i < nrows;
-  double g[4][8];
+  double g[CPT][8];
 #pragma unroll
-  for (int c = 0; c < 4; ++c)
+  for (int c = 0; c < CPT; ++c)
 #pragma unroll
     for (int q = 0; q < 8; ++q) g[c][q] = (rok && q < E1 && j0 + c < r) ? Gs[(i * E1 + q) * r + j0 + c] : 0.0;
-  const int tc = r - j0;   // the t column among this thread's four (0..3), if any
+  const int tc = r - j0;   // the t column among this thread's columns (0..CPT-1), if any
   double* ob = out + ((p0 + half) * (int64_t)cpad + j0) * ld + row;
-  const int64_t ostep = 2 * (int64_t)cpad * ld;
+  const int64_t ostep = NH * (int64_t)cpad * ld;
   const double2* c2 = reinterpret_cast<const double2*>(cs) + half * 4 * kWyRB + i;
   const double* tp = t + (p0 + half) * t_stride + row;
 #pragma unroll 2
-  for (int pl = half; pl < np; pl += 2) {
-    double m[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int pl = half; pl < np; pl += NH) {
+    double m[CPT];
+#pragma unroll
+    for (int cc = 0; cc < CPT; ++cc) m[cc] = 0.0;
 #pragma unroll
     for (int q2 = 0; q2 < 4; ++q2) {
       const double2 c = c2[q2 * kWyRB];
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
+      for (int cc = 0; cc < CPT; ++cc) {
         if (2 * q2 < E1) m[cc] = fma(c.x, g[cc][2 * q2], m[cc]);
         if (2 * q2 + 1 < E1) m[cc] = fma(c.y, g[cc][2 * q2 + 1], m[cc]);
       }
     }
-    if (!rok) m[0] = m[1] = m[2] = m[3] = 0.0;   // padding rows (their coefficient slots are not initialised)
-    if (tc >= 0 && tc < 4) {
+    if (!rok) {   // padding rows (their coefficient slots are not initialised)
+#pragma unroll
+      for (int cc = 0; cc < CPT; ++cc) m[cc] = 0.0;
+    }
+    if (tc >= 0 && tc < CPT) {
       const double tv = rok ? *tp : 0.0;
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc)
+      for (int cc = 0; cc < CPT; ++cc)
         if (cc == tc) m[cc] = tv;
     }
 #pragma unroll
-    for (int cc = 0; cc < 4; ++cc)
+    for (int cc = 0; cc < CPT; ++cc)
       if (j0 + cc < cpad) ob[cc * ld] = m[cc];
     ob += ostep;
-    c2 += 2 * 4 * kWyRB;
-    tp += 2 * t_stride;
+    c2 += NH * 4 * kWyRB;
+    tp += NH * t_stride;
   }
 }
 

@@ -22,7 +22,9 @@
 #include "k_lsq_sm.cuh"
 #include "k_lsq_wy.cuh"
 #include "k_tsqr.cuh"
+#include "k_select.cuh"
 #include "k_cg.cuh"
+#include "k_bicg.cuh"
 #include "k_gauss.cuh"
 #include "k_recon.cuh"
 
@@ -1517,6 +1519,44 @@ extern "C" int sas_tsqr_r(const void* A, int64_t m, int32_t w, int32_t dtype, vo
   return tsqr_t<cplx, 4, 16>((const cplx*)A, m, w, (cplx*)R, st);
 }
 
+// ---------------------------------------------------------------------------
+// Leverage selector: Q = A C and the squared row norms of Q (k_select.cuh).
+template <typename T>
+static int range_rows_t(const T* A, int64_t m, int w, const T* Chost, int k, T* Q, double* scores, int device,
+                        cudaStream_t st) {
+  const size_t smem = range_rows_smem_bytes<T>(w, k);
+  if (int rc = smem_optin<k_range_rows<T>>(false)) return rc;
+  T* Cd = nullptr;
+  SAS_CUDA_CHECK(cudaMallocAsync((void**)&Cd, (size_t)w * k * sizeof(T), st));
+  SAS_CUDA_CHECK(cudaMemcpyAsync(Cd, Chost, (size_t)w * k * sizeof(T), cudaMemcpyHostToDevice, st));
+  int sms = 0;
+  SAS_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  int occ = 0;
+  SAS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_range_rows<T>, 256, smem));
+  if (occ < 1) {
+    sas_set_error("sas_range_rows: tile does not fit (w=%d k=%d smem=%zu)", w, k, smem);
+    return SAS_ERR_ARG;
+  }
+  int64_t grid = std::min<int64_t>((m + kSelRows - 1) / kSelRows, (int64_t)sms * occ);
+  k_range_rows<T><<<(unsigned)grid, 256, smem, st>>>(A, m, w, Cd, k, Q, scores);
+  SAS_CUDA_CHECK(cudaGetLastError());
+  SAS_CUDA_CHECK(cudaFreeAsync(Cd, st));
+  return SAS_OK;
+}
+
+extern "C" int sas_range_rows(const void* A, int64_t m, int32_t w, const void* C, int32_t k, int32_t dtype, void* Q,
+                              double* scores, int32_t device, void* stream) {
+  ARG_CHECK(A && C && (Q || scores), "sas_range_rows: null pointer");
+  ARG_CHECK(m >= 1 && w >= 1 && w <= 64 && k >= 1 && k <= w,
+            "sas_range_rows: need m >= 1, 1 <= k <= w <= 64 (m=%lld w=%d k=%d)", (long long)m, w, k);
+  ARG_CHECK(dtype == SAS_F64 || dtype == SAS_C128, "sas_range_rows: dtype must be SAS_F64 or SAS_C128");
+  DevGuard g(device);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == SAS_F64)
+    return range_rows_t<double>((const double*)A, m, w, (const double*)C, k, (double*)Q, scores, device, st);
+  return range_rows_t<cplx>((const cplx*)A, m, w, (const cplx*)C, k, (cplx*)Q, scores, device, st);
+}
+
 
 // ---------------------------------------------------------------------------
 // Jacobi-preconditioned CG for the stencil snapshot solves (k_cg.cuh).
@@ -1594,4 +1634,91 @@ extern "C" int sas_cg_stencil(int64_t n, int32_t E, const double* dg, const doub
   cudaFreeAsync(ppq, st);
   SAS_CUDA_CHECK(cudaStreamSynchronize(st));
   return SAS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Jacobi-preconditioned BiCGSTAB on a CSR matrix (k_bicg.cuh).
+template <typename T>
+static int bicgstab_t(int64_t n, const int32_t* rp, const int32_t* ci, const T* va, const T* dg, const T* b, T* x,
+                      double tol, double a_norm, int maxiter, int check_every, int device, cudaStream_t st,
+                      int32_t* iters_out, double* rnorm_out, double* xnorm_out) {
+  int sms = 0;
+  SAS_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  const int nb = (int)std::min<int64_t>((n + kCgThreads - 1) / kCgThreads, (int64_t)sms * 8);
+  T* vec = nullptr;          // r, rhat, p, v, s, t, phat, shat
+  double* part = nullptr;    // three partial blocks: x-step, v-step, t-step
+  BicgScal<T>* scal = nullptr;
+  SAS_CUDA_CHECK(cudaMallocAsync((void**)&vec, 8 * (size_t)n * sizeof(T), st));
+  SAS_CUDA_CHECK(cudaMallocAsync((void**)&part, 3 * (size_t)nb * kBicgPart * sizeof(double), st));
+  SAS_CUDA_CHECK(cudaMallocAsync((void**)&scal, 2 * sizeof(BicgScal<T>), st));
+  T *r = vec, *rhat = vec + n, *p = vec + 2 * n, *v = vec + 3 * n, *s = vec + 4 * n, *t = vec + 5 * n,
+    *phat = vec + 6 * n, *shat = vec + 7 * n;
+  double *part_x = part, *part_v = part + (size_t)nb * kBicgPart, *part_t = part + 2 * (size_t)nb * kBicgPart;
+  std::vector<double> hp((size_t)nb * kBicgPart);
+  auto host_sums = [&](const double* dpart, double* s4, double* s5) -> int {
+    SAS_CUDA_CHECK(cudaMemcpyAsync(hp.data(), dpart, hp.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+    SAS_CUDA_CHECK(cudaStreamSynchronize(st));
+    double a4 = 0.0, a5 = 0.0;
+    for (int i = 0; i < nb; ++i) {
+      a4 += hp[(size_t)i * kBicgPart + 4];
+      a5 += hp[(size_t)i * kBicgPart + 5];
+    }
+    *s4 = a4;
+    *s5 = a5;
+    return SAS_OK;
+  };
+  int rc = SAS_OK;
+  k_bicg_init<T><<<nb, kCgThreads, 0, st>>>(n, b, x, r, rhat, p, v, part_x, scal);
+  double bn2 = 0.0, dummy = 0.0;
+  if ((rc = host_sums(part_x, &bn2, &dummy))) return rc;
+  const double bn = sqrt(bn2);
+  int it = 0;
+  for (it = 0; it < maxiter; ++it) {
+    BicgScal<T>* cur = scal + (it & 1);
+    const BicgScal<T>* prev = scal + ((it + 1) & 1);
+    k_bicg_p<T><<<nb, kCgThreads, 0, st>>>(n, dg, r, v, p, phat, part_x, prev, cur);
+    k_bicg_spmv<T, 0><<<nb, kCgThreads, 0, st>>>(n, rp, ci, va, phat, rhat, v, part_v);
+    k_bicg_s<T><<<nb, kCgThreads, 0, st>>>(n, dg, r, v, s, shat, part_v, cur);
+    k_bicg_spmv<T, 1><<<nb, kCgThreads, 0, st>>>(n, rp, ci, va, shat, s, t, part_t);
+    k_bicg_x<T><<<nb, kCgThreads, 0, st>>>(n, rhat, phat, shat, s, t, x, r, part_t, cur, part_x);
+    if ((it + 1) % check_every == 0 || it + 1 == maxiter) {
+      double rr = 0.0, xx = 0.0;
+      if ((rc = host_sums(part_x, &rr, &xx))) return rc;
+      const double rn = sqrt(rr);
+      if (!std::isfinite(rn) || rn <= tol * bn || rn <= 1e-12 * (a_norm * sqrt(xx) + bn)) {
+        ++it;
+        break;
+      }
+    }
+  }
+  SAS_CUDA_CHECK(cudaGetLastError());
+  // the true residual b - A x
+  k_bicg_spmv<T, 2><<<nb, kCgThreads, 0, st>>>(n, rp, ci, va, x, b, nullptr, part_v);
+  double rr = 0.0, xx = 0.0;
+  if ((rc = host_sums(part_v, &rr, &xx))) return rc;
+  if (iters_out) *iters_out = it;
+  if (rnorm_out) *rnorm_out = sqrt(rr);
+  if (xnorm_out) *xnorm_out = sqrt(xx);
+  SAS_CUDA_CHECK(cudaFreeAsync(vec, st));
+  SAS_CUDA_CHECK(cudaFreeAsync(part, st));
+  SAS_CUDA_CHECK(cudaFreeAsync(scal, st));
+  return SAS_OK;
+}
+
+extern "C" int sas_bicgstab_csr(int64_t n, const int32_t* rowptr, const int32_t* colind, const void* val,
+                                const void* diag, const void* b, void* x, int32_t dtype, double tol, double a_norm,
+                                int32_t maxiter, int32_t check_every, int32_t device, void* stream,
+                                int32_t* iters_out, double* rnorm_out, double* xnorm_out) {
+  ARG_CHECK(n >= 1 && n < (int64_t)1 << 31, "sas_bicgstab_csr: need 1 <= n < 2^31");
+  ARG_CHECK(rowptr && colind && val && diag && b && x, "sas_bicgstab_csr: null device pointer");
+  ARG_CHECK(dtype == SAS_F64 || dtype == SAS_C128, "sas_bicgstab_csr: dtype must be SAS_F64 or SAS_C128");
+  ARG_CHECK(maxiter >= 1 && check_every >= 1, "sas_bicgstab_csr: maxiter and check_every must be >= 1");
+  DevGuard g(device);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == SAS_F64)
+    return bicgstab_t<double>(n, rowptr, colind, (const double*)val, (const double*)diag, (const double*)b,
+                              (double*)x, tol, a_norm, maxiter, check_every, device, st, iters_out, rnorm_out,
+                              xnorm_out);
+  return bicgstab_t<cplx>(n, rowptr, colind, (const cplx*)val, (const cplx*)diag, (const cplx*)b, (cplx*)x, tol,
+                          a_norm, maxiter, check_every, device, st, iters_out, rnorm_out, xnorm_out);
 }

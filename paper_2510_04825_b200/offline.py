@@ -206,55 +206,43 @@ def _stencil_cg(system, p, device, tol=1e-11, maxiter=50_000, tensors=None):
 def _affine_bicgstab(system, p, device, tol=1e-11, maxiter=40_000):
     """Jacobi-preconditioned BiCGSTAB on the GPU for a large affine (possibly
     complex, non-symmetric) A(p) = sum_k f_k(p) A_k (config 4's transfer-function
-    sweep), in place of the reference's SuperLU solve (systems.py:187-222).
+    sweep), in place of the reference's SuperLU solve (systems.py:187-222), by
+    libsas's fused BiCGSTAB kernels (k_bicg.cuh, sas_bicgstab_csr: direction
+    update, CSR SpMV with its dot products, vector updates; device-side
+    fixed-order reductions, no host round trip between iterations).
     Stops at ||r|| <= tol ||b|| or, if fp64 cannot attain that, once the
     reference's full_solve guard ||r|| <= 1e-10 (||A|| ||x|| + ||b||) holds
     with a 100x margin; the guard is checked on the true residual."""
+    import ctypes as C
+
     import torch
+
+    from . import _capi
     a = system.matrix(p).tocsr()
+    a.sort_indices()
     b_np = np.asarray(system.full_rhs(p))
-    dt = torch.complex128 if (np.iscomplexobj(a.data) or np.iscomplexobj(b_np)) else torch.float64
-    npdt = np.complex128 if dt == torch.complex128 else np.float64
-    A = torch.sparse_csr_tensor(torch.from_numpy(a.indptr.astype(np.int64)), torch.from_numpy(a.indices.astype(np.int64)),
-                                torch.from_numpy(a.data.astype(npdt)), size=a.shape, device=device,
-                                check_invariants=True)
-    d = torch.from_numpy(a.diagonal().astype(npdt)).to(device)
-    b = torch.from_numpy(b_np.astype(npdt)).to(device)
+    cplx_ = np.iscomplexobj(a.data) or np.iscomplexobj(b_np)
+    npdt = np.complex128 if cplx_ else np.float64
+    if a.nnz >= 2 ** 31:
+        raise ConfigError("BiCGSTAB snapshot solve: nnz above 2^31")
+    dev = torch.device(device)
+    up = lambda arr: torch.from_numpy(np.ascontiguousarray(arr)).to(dev)
+    rp, ci, va = up(a.indptr.astype(np.int32)), up(a.indices.astype(np.int32)), up(a.data.astype(npdt))
+    d, b = up(a.diagonal().astype(npdt)), up(b_np.astype(npdt))
+    x = torch.empty_like(b)
     a_norm = float(spla.norm(a))
-    bn = float(torch.linalg.norm(b))
-
-    def mv(v):
-        return torch.mv(A, v)
-
-    x = torch.zeros_like(b)
-    r = b.clone()
-    rhat = r.clone()
-    rho = alpha = omega = torch.ones((), dtype=dt, device=device)
-    v = torch.zeros_like(b)
-    pd = torch.zeros_like(b)
-    for it in range(maxiter):
-        rho_new = torch.vdot(rhat, r)
-        beta = (rho_new / rho) * (alpha / omega)
-        pd = r + beta * (pd - omega * v)
-        phat = pd / d
-        v = mv(phat)
-        alpha = rho_new / torch.vdot(rhat, v)
-        s = r - alpha * v
-        shat = s / d
-        t = mv(shat)
-        omega = torch.vdot(t, s) / torch.vdot(t, t)
-        x += alpha * phat + omega * shat
-        r = s - omega * t
-        rho = rho_new
-        if it % 25 == 0:
-            rn = float(torch.linalg.norm(r))
-            if not np.isfinite(rn):
-                break
-            if rn <= tol * bn or rn <= 1e-12 * (a_norm * float(torch.linalg.norm(x)) + bn):
-                break
-    xh = x.cpu().numpy()
-    _guard(lambda w: a @ w, a_norm, xh, b_np, p)
-    return xh
+    bn = float(np.linalg.norm(b_np))
+    its, rn, xn = C.c_int32(0), C.c_double(0.0), C.c_double(0.0)
+    lib = _capi.load()
+    st = torch.cuda.current_stream(dev)
+    _capi.check(lib.sas_bicgstab_csr(a.shape[0], _capi.ptr(rp), _capi.ptr(ci), _capi.ptr(va), _capi.ptr(d),
+                                     _capi.ptr(b), _capi.ptr(x), _capi.SAS_C128 if cplx_ else _capi.SAS_F64, tol,
+                                     a_norm, maxiter, 25, int(dev.index or 0), C.c_void_p(st.cuda_stream),
+                                     C.byref(its), C.byref(rn), C.byref(xn)), "sas_bicgstab_csr")
+    if not math.isfinite(rn.value) or rn.value > FULL_SOLVE_RTOL * max(a_norm * xn.value + bn, 1e-300):
+        raise NumericalError(f"full_solve residual {rn.value:.3e} exceeds {FULL_SOLVE_RTOL:.0e} * "
+                             f"(||A|| ||x|| + ||b||) at p={p} (BiCGSTAB, {its.value} iterations)")
+    return x.cpu().numpy()
 
 
 def snapshot_solves(system, points, device=None, prefer_cg: bool = False):
@@ -355,12 +343,98 @@ def leverage_scores(q) -> np.ndarray:
     return np.einsum("ij,ij->i", q.conj(), q).real
 
 
+def leverage_scores_gpu(target, device=0, rtol=1e-12, max_passes=4):
+    """Leverage scores of the numerical range of a tall `target` on the GPU with
+    libsas kernels (subsample.py:84-94 + 144-159 without the n x w host SVD):
+
+      R = TSQR(target)                      sas_tsqr_r (column norms = ||R[:, j]||)
+      R diag(1/norms) = U S V^H             w x w host SVD; keep s_j > rtol s_0
+      C = diag(1/norms) V_k S_k^-1          so that W = target C = U_k in exact arithmetic
+      repeat: (W, scores) = range_rows(target, C); R2 = TSQR(W);
+              done if ||R2^H R2 - I|| <= 1e-10, else C <- C R2^-1
+
+    W from the first pass is orthonormal only to eps s_0 / s_k; one more pass
+    brings it to rounding.  The final ||W^H W - I|| takes the place of the
+    reference's 1e-8 orthonormality check.  The scores are those of the SAME
+    subspace the reference's thin SVD spans; they agree with it to the
+    conditioning of that subspace (about eps s_0 / s_k), not bit for bit.
+    Returns (scores as a CUDA tensor, kept rank)."""
+    import ctypes as C_
+    import torch
+    from . import _capi
+    dev = torch.device(f"cuda:{device}" if isinstance(device, int) else device)
+    A = target if isinstance(target, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(target))
+    A = A.to(dev).contiguous()
+    m, w = A.shape
+    if w > 64:
+        raise ConfigError("leverage_scores_gpu: width above 64")
+    lib = _capi.load()
+    dt = _capi.SAS_C128 if A.is_complex() else _capi.SAS_F64
+    npdt = np.complex128 if A.is_complex() else np.float64
+    st = C_.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    di = int(dev.index or 0)
+
+    def tsqr(M):
+        R = torch.empty((M.shape[1], M.shape[1]), dtype=M.dtype, device=dev)
+        _capi.check(lib.sas_tsqr_r(_capi.ptr(M), M.shape[0], M.shape[1], dt, _capi.ptr(R), di, st), "sas_tsqr_r")
+        return np.triu(R.cpu().numpy())
+
+    R = tsqr(A)
+    norms = np.linalg.norm(R, axis=0)
+    norms = np.where(norms == 0, 1.0, norms)
+    _, sv, vh = np.linalg.svd(R / norms)
+    if sv[0] == 0:
+        raise RankDeficiencyError("zero matrix has no range basis")
+    keep = max(int(np.count_nonzero(sv > rtol * sv[0])), 1)
+    Cm = (vh[:keep].conj().T / sv[:keep]) / norms[:, None]
+    scores = torch.empty(m, dtype=torch.float64, device=dev)
+    W = torch.empty((m, keep), dtype=A.dtype, device=dev)
+    err = np.inf
+    for _ in range(max_passes):
+        Ch = np.ascontiguousarray(Cm, dtype=npdt)
+        _capi.check(lib.sas_range_rows(_capi.ptr(A), m, w, Ch.ctypes.data_as(C_.c_void_p), keep, dt, _capi.ptr(W),
+                                       _capi.ptr(scores), di, st), "sas_range_rows")
+        R2 = tsqr(W)
+        err = float(np.linalg.norm(R2.conj().T @ R2 - np.eye(keep)))
+        if err <= 1e-10:
+            break
+        Cm = np.linalg.solve(R2.T, Cm.T).T    # C R2^-1
+    if not err <= 1e-8:
+        raise ValueError("leverage_scores needs orthonormal columns")
+    return scores, keep
+
+
 def select_rows(b, rhs=None, strategy="leverage", oversample=4.0, augment_rhs=True, seed=0,
-                rng=None, anchors=()) -> RowSelector:
-    b = np.asarray(b)
+                rng=None, anchors=(), device=None) -> RowSelector:
+    """device=None: the host restatement (bit-identical to the reference's S and
+    weights).  device=<cuda>: the leverage scores come from the GPU kernels
+    (leverage_scores_gpu); the draw itself (numpy's rng.choice on the n
+    probabilities) stays the reference's."""
+    b_t = b if device is not None and not isinstance(b, np.ndarray) else None
+    if b_t is None:
+        b = np.asarray(b)
     n, _ = b.shape
     if rng is None:
         rng = np.random.default_rng(seed)
+    if device is not None and strategy == "leverage":
+        import torch
+        bt = b_t if b_t is not None else torch.from_numpy(np.ascontiguousarray(b))
+        bt = bt.to(device)
+        if augment_rhs and rhs is not None:
+            rt = torch.as_tensor(np.asarray(rhs)).to(device)
+            dtp = torch.promote_types(bt.dtype, rt.dtype)
+            bt = torch.cat([bt.to(dtp), rt.to(dtp)[:, None]], dim=1)
+        width = bt.shape[1]
+        s = int(math.ceil(oversample * width))
+        scores_t, _ = leverage_scores_gpu(bt, device=device)
+        scores = scores_t.cpu().numpy()
+        total = scores.sum()
+        if total <= 0:
+            raise RankDeficiencyError("all-zero leverage scores")
+        pi = scores / total
+        idx = rng.choice(n, size=s, replace=True, p=pi)
+        weights = 1.0 / np.sqrt(s * pi[idx])
+        return RowSelector(indices=idx, n=n, weights=weights, strategy=strategy, anchors=tuple(anchors))
     target = b
     if augment_rhs and rhs is not None:
         target = np.column_stack([b, np.asarray(rhs)])
@@ -411,9 +485,12 @@ def anchor_product(system, anchor, basis, device=None) -> np.ndarray:
     return np.asarray(system.matrix(anchor) @ X)
 
 
-def offline(problem, device=None, prefer_cg=False, basis: Optional[SnapshotBasis] = None):
+def offline(problem, device=None, prefer_cg=False, basis: Optional[SnapshotBasis] = None,
+            gpu_select: bool = False):
     """Full offline recipe of a problems.Problem: snapshot basis, anchor,
-    leverage selector with `samples` rows (cli.py:239-265)."""
+    leverage selector with `samples` rows (cli.py:239-265).  gpu_select: the
+    selector's leverage scores from the GPU kernels (select_rows(device=...))
+    instead of the host thin SVD."""
     system = problem.system
     if basis is None:
         basis = build_snapshot(system, problem.snapshot_points, problem.snapshot_mode, device=device,
@@ -423,7 +500,8 @@ def offline(problem, device=None, prefer_cg=False, basis: Optional[SnapshotBasis
     rhs_anchor = system.full_rhs(anchor)
     width = basis.rank + 1
     sel = select_rows(b_anchor, rhs_anchor, strategy="leverage", oversample=problem.samples / width,
-                      seed=problem.selector_seed, anchors=(anchor,))
+                      seed=problem.selector_seed, anchors=(anchor,),
+                      device=(device if gpu_select and device is not None else None))
     if sel.size != problem.samples:
         raise ConfigError(f"selector size {sel.size} != requested samples {problem.samples}")
     return basis, sel

@@ -61,3 +61,45 @@ def test_gpu_cg_snapshot_matches_reference_full_solve(cfg, kw):
         bound = 4 * cond * (r_gpu + r_ref) / np.linalg.norm(b)
         rel = np.linalg.norm(x_gpu - x_ref) / np.linalg.norm(x_ref)
         assert rel <= max(bound, 1e-13), (cfg, p, rel, bound)
+
+
+@pytest.mark.parametrize("grid", [60, 150])
+def test_gpu_bicgstab_snapshot_matches_direct_solve(grid):
+    """config 4's snapshot solver (k_bicg.cuh, sas_bicgstab_csr) against the
+    reference's direct sparse solve with its residual guard (systems.py:187-222),
+    complex non-symmetric A(p) = A0 + p I at small grids."""
+    from paper_2510_04825_b200.offline import _affine_bicgstab, _sparse_solve
+    prob = problems.convdiff_tf(grid=grid)
+    s = prob.system
+    for p in (1e-2j, 1.0j, 1e2j):
+        x = _affine_bicgstab(s, p, "cuda:0")
+        y = _sparse_solve(s.matrix(p), s.full_rhs(p), p)
+        assert np.linalg.norm(x - y) <= 1e-10 * np.linalg.norm(y)
+        x2 = _affine_bicgstab(s, p, "cuda:0")      # fixed-order reductions: same bits
+        assert np.array_equal(x, x2)
+
+
+def test_gpu_bicgstab_real_system():
+    """The real-dtype instantiation on a real non-symmetric system."""
+    import ctypes as C
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spla
+    from paper_2510_04825_b200 import _capi
+    a = (problems.convdiff_matrix(50) + 3.0 * sp.identity(2500)).tocsr()
+    a.sort_indices()
+    rng = np.random.default_rng(2)
+    b = rng.standard_normal(2500)
+    up = lambda v: torch.from_numpy(np.ascontiguousarray(v)).cuda()
+    rp, ci, va, d, bt = up(a.indptr.astype(np.int32)), up(a.indices.astype(np.int32)), up(a.data), up(a.diagonal()), up(b)
+    x = torch.empty_like(bt)
+    its, rn, xn = C.c_int32(0), C.c_double(0.0), C.c_double(0.0)
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    _capi.check(_capi.load().sas_bicgstab_csr(2500, _capi.ptr(rp), _capi.ptr(ci), _capi.ptr(va), _capi.ptr(d),
+                                              _capi.ptr(bt), _capi.ptr(x), _capi.SAS_F64, 1e-12, float(spla.norm(a)),
+                                              5000, 10, 0, st, C.byref(its), C.byref(rn), C.byref(xn)), "bicgstab")
+    y = spla.spsolve(a.tocsc(), b)
+    xh = x.cpu().numpy()
+    assert 0 < its.value < 5000
+    assert np.linalg.norm(xh - y) <= 1e-9 * np.linalg.norm(y)
+    assert abs(rn.value - np.linalg.norm(b - a @ xh)) <= 1e-12 * np.linalg.norm(b) + 1e-3 * rn.value
+    assert abs(xn.value - np.linalg.norm(xh)) <= 1e-12 * np.linalg.norm(xh)

@@ -184,16 +184,3 @@ def test_estimate_residual_formula():
     plan2 = dataclasses.replace(plan, selector=unweighted)
     with pytest.raises(ValueError):
         online.estimate_residual(plan2, sol)
-
-
-def test_affine_bicgstab_matches_direct_solve():
-    # config 4's snapshot solver (GPU BiCGSTAB on large grids) against the
-    # reference's direct sparse solve, here on the CPU at a small grid
-    from paper_2510_04825_b200 import problems
-    from paper_2510_04825_b200.offline import _affine_bicgstab, _sparse_solve
-    prob = problems.convdiff_tf(grid=60)
-    s = prob.system
-    for p in (1e-2j, 1.0j, 1e2j):
-        x = _affine_bicgstab(s, p, "cpu")
-        y = _sparse_solve(s.matrix(p), s.full_rhs(p), p)
-        assert np.linalg.norm(x - y) <= 1e-10 * np.linalg.norm(y)
