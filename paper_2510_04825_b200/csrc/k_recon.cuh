@@ -368,3 +368,104 @@ __global__ void __launch_bounds__(256, 2) k_resid_stencil_blk(const double* __re
   if (threadIdx.x == 0)
     for (int u = 0; u < npb; ++u) part[((pb + u) * gridDim.x + blockIdx.x) * 3 + 1] = tbb;
 }
+
+// K6, warp-per-node form for compile-time (E, DP) (configs 3 and 5: (4, 4) and
+// (6, 6)): lane l owns parameter values 2l, 2l+1 of the 64-parameter block, so a
+// node's x block is ONE coalesced 512-byte read per warp, the per-parameter sums
+// never cross lanes, and the fully unrolled edge loop puts all neighbour indices,
+// neighbour x blocks and E exp chains per parameter value in flight (the generic
+// kernel above walks the edges one dependent L2 round trip at a time).  The
+// exponent is formed in exp-table units (the lane's parameter values are scaled
+// by 2048 / ln 2 once), 1 / h^2 is applied once per node: 7 + DP + 4 FP64-pipe
+// operations per edge coefficient instead of 10 + DP + 4.  Same partials.
+template <int E, int DP>
+__global__ void __launch_bounds__(256, 2) k_resid_stencil_w(const double* __restrict__ x, int64_t n, int64_t P,
+                                                            const int32_t* __restrict__ nbr,
+                                                            const double* __restrict__ phi, double hh,
+                                                            const double* __restrict__ b,
+                                                            const double* __restrict__ params,
+                                                            double* __restrict__ part) {
+  static_assert(kResidPB == 64, "one warp = 64 parameter values");
+  __shared__ double red[32];
+  __shared__ double tab_s[2048];
+  __shared__ double rsum[kResidPB][8];
+  __shared__ double asum[kResidPB][8];
+  for (int j = threadIdx.x; j < 2048; j += blockDim.x) tab_s[j] = g_exp2_tab2048[j];
+  __syncthreads();
+  const double inv_hh = 1.0 / hh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t pb = (int64_t)blockIdx.y * kResidPB;
+  const int npb = (int)((P - pb) < kResidPB ? (P - pb) : kResidPB);
+  double pu[2][DP];
+#pragma unroll
+  for (int u = 0; u < 2; ++u)
+#pragma unroll
+    for (int k = 0; k < DP; ++k)
+      pu[u][k] = (2 * lane + u < npb) ? params[(pb + 2 * lane + u) * DP + k] * SAS_INVLN2X2K : 0.0;
+  const double2* xb = reinterpret_cast<const double2*>(x + (int64_t)blockIdx.y * n * kResidPB) + lane;
+  double rr[2] = {0.0, 0.0}, aa[2] = {0.0, 0.0}, bb = 0.0;
+  const int64_t nstride = (int64_t)gridDim.x * 8;
+  for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < n; i += nstride) {
+    int m[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) m[e] = __ldg(nbr + i * E + e);
+    const double2 xi = __ldg(xb + i * (kResidPB / 2));
+    double2 xm[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) xm[e] = (m[e] >= 0) ? __ldg(xb + (int64_t)m[e] * (kResidPB / 2)) : make_double2(0.0, 0.0);
+    const double bi = __ldg(b + i);
+    double acc[2] = {0.0, 0.0}, ab[2] = {0.0, 0.0};
+    const double axi[2] = {fabs(xi.x), fabs(xi.y)};
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      double phv[DP];
+#pragma unroll
+      for (int k = 0; k < DP; ++k) phv[k] = __ldg(phi + (i * E + e) * DP + k);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        double arg = pu[u][0] * phv[0];
+#pragma unroll
+        for (int k = 1; k < DP; ++k) arg = fma(pu[u][k], phv[k], arg);
+        // e^(arg ln2 / 2048): k = rint(arg), r = arg - k, table 2^(k mod 2048 / 2048), degree-3 tail
+        const double kd = arg + SAS_EXP_MAGIC;
+        const int ki = __double2loint(kd);
+        const double r = arg - (kd - SAS_EXP_MAGIC);
+        double q = fma(r, SAS_EXP2K_A3, SAS_EXP2K_A2);
+        q = fma(q, r, SAS_EXP2K_A1);
+        q = q * r;
+        const double t = tab_s[ki & 2047];
+        const double res = fma(t, q, t);
+        const int keep = (ki >= SAS_EXP2K_KMIN) ? -1 : 0;
+        const double c = __hiloint2double((__double2hiint(res) + ((ki >> 11) << 20)) & keep, __double2loint(res) & keep);
+        const double xv = u ? xi.y : xi.x, xn = u ? xm[e].y : xm[e].x;
+        acc[u] = fma(c, xv - xn, acc[u]);
+        ab[u] = fma(c, axi[u] + fabs(xn), ab[u]);   // |A| |x|: c_e > 0
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const double res = fma(acc[u], inv_hh, -bi);
+      const double av = ab[u] * inv_hh;
+      rr[u] = fma(res, res, rr[u]);
+      aa[u] = fma(av, av, aa[u]);
+    }
+    bb = fma(bi, bi, bb);
+  }
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    rsum[2 * lane + u][warp] = rr[u];
+    asum[2 * lane + u][warp] = aa[u];
+  }
+  const double tbb = block_sum(lane == 0 ? bb : 0.0, red);  // (its __syncthreads also publishes rsum)
+  if (threadIdx.x < npb) {
+    double t = 0.0, ta = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      t += rsum[threadIdx.x][w];
+      ta += asum[threadIdx.x][w];
+    }
+    part[((pb + threadIdx.x) * gridDim.x + blockIdx.x) * 3] = t;
+    part[((pb + threadIdx.x) * gridDim.x + blockIdx.x) * 3 + 2] = ta;
+  }
+  if (threadIdx.x == 0)
+    for (int u = 0; u < npb; ++u) part[((pb + u) * gridDim.x + blockIdx.x) * 3 + 1] = tbb;
+}
