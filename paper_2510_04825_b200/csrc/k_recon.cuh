@@ -369,10 +369,6 @@ __global__ void __launch_bounds__(256, 2) k_resid_stencil_blk(const double* __re
     for (int u = 0; u < npb; ++u) part[((pb + u) * gridDim.x + blockIdx.x) * 3 + 1] = tbb;
 }
 
-__device__ __forceinline__ void l2_prefetch(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
-}
-
 // K6, warp-per-node form for compile-time (E, DP) (configs 3 and 5: (4, 4) and
 // (6, 6)): lane l owns parameter values 2l, 2l+1 of the 64-parameter block, so a
 // node's x block is ONE coalesced 512-byte read per warp, the per-parameter sums
@@ -382,6 +378,8 @@ __device__ __forceinline__ void l2_prefetch(const void* p) {
 // exponent is formed in exp-table units (the lane's parameter values are scaled
 // by 2048 / ln 2 once), 1 / h^2 is applied once per node: 7 + DP + 4 FP64-pipe
 // operations per edge coefficient instead of 10 + DP + 4.  Same partials.
+// (Neighbour indices two nodes ahead + L2 prefetches of the next node's blocks: measured
+// slower, 0.208 vs 0.195 s on config 5 - profiles/r02e/r02e_resid_pf.jsonl.)
 template <int E, int DP>
 __global__ void __launch_bounds__(256, 2) k_resid_stencil_w(const double* __restrict__ x, int64_t n, int64_t P,
                                                             const int32_t* __restrict__ nbr,
@@ -409,27 +407,10 @@ __global__ void __launch_bounds__(256, 2) k_resid_stencil_w(const double* __rest
   const double2* xb = reinterpret_cast<const double2*>(x + (int64_t)blockIdx.y * n * kResidPB) + lane;
   double rr[2] = {0.0, 0.0}, aa[2] = {0.0, 0.0}, bb = 0.0;
   const int64_t nstride = (int64_t)gridDim.x * 8;
-  // two nodes ahead: the neighbour indices; one node ahead: L2 prefetches of its x blocks,
-  // its neighbours' x blocks and its phi rows (the +stride neighbour and phi are first touches)
-  const int64_t i00 = (int64_t)blockIdx.x * 8 + warp;
-  int mb[E];
-#pragma unroll
-  for (int e = 0; e < E; ++e) mb[e] = (i00 + nstride < n) ? __ldg(nbr + (i00 + nstride) * E + e) : -1;
-  for (int64_t i = i00; i < n; i += nstride) {
+  for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < n; i += nstride) {
     int m[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) m[e] = __ldg(nbr + i * E + e);
-    if (i + nstride < n) {
-      const int64_t i1 = i + nstride;
-      l2_prefetch(xb + i1 * (kResidPB / 2));
-#pragma unroll
-      for (int e = 0; e < E; ++e)
-        if (mb[e] >= 0) l2_prefetch(xb + (int64_t)mb[e] * (kResidPB / 2));
-      if (lane * 16 < E * DP) l2_prefetch(phi + i1 * E * DP + lane * 16);
-      const bool two = i1 + nstride < n;
-#pragma unroll
-      for (int e = 0; e < E; ++e) mb[e] = two ? __ldg(nbr + (i1 + nstride) * E + e) : -1;
-    }
     const double2 xi = __ldg(xb + i * (kResidPB / 2));
     double2 xm[E];
 #pragma unroll
