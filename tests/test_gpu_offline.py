@@ -103,3 +103,13 @@ def test_gpu_bicgstab_real_system():
     assert np.linalg.norm(xh - y) <= 1e-9 * np.linalg.norm(y)
     assert abs(rn.value - np.linalg.norm(b - a @ xh)) <= 1e-12 * np.linalg.norm(b) + 1e-3 * rn.value
     assert abs(xn.value - np.linalg.norm(xh)) <= 1e-12 * np.linalg.norm(xh)
+
+
+def test_gpu_bicgstab_residual_guard_raises():
+    """A snapshot solve that has not converged raises the reference's NumericalError
+    (full_solve's residual guard, systems.py:205-221) instead of returning x."""
+    from paper_2510_04825_b200.errors import NumericalError
+    from paper_2510_04825_b200.offline import _affine_bicgstab
+    prob = problems.convdiff_tf(grid=60)
+    with pytest.raises(NumericalError):
+        _affine_bicgstab(prob.system, 1e-2j, "cuda:0", maxiter=3)

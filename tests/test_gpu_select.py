@@ -105,3 +105,33 @@ def test_leverage_scores_gpu_full_size_config3_shape():
     assert gk == hk == 41
     assert abs(gs.sum() - 41) <= 1e-8
     assert np.abs(gs - hs).max() <= 1e-6 * hs.max()
+
+
+def test_leverage_scores_gpu_error_behaviour():
+    """The reference's errors (subsample.py:154-155; select_rows' all-zero guard) and the C ABI's argument checks."""
+    from paper_2510_04825_b200.errors import RankDeficiencyError
+    with pytest.raises(RankDeficiencyError):
+        offline.leverage_scores_gpu(np.zeros((500, 7)), device=0)
+    lib = _capi.load()
+    A = torch.zeros((10, 4), dtype=torch.float64, device="cuda")
+    c = np.zeros((4, 5))
+    sc = torch.empty(10, dtype=torch.float64, device="cuda")
+    rc = lib.sas_range_rows(_capi.ptr(A), 10, 4, c.ctypes.data_as(C.c_void_p), 5, _capi.SAS_F64, None, _capi.ptr(sc), 0,
+                            C.c_void_p(0))
+    assert rc != 0 and "k <= w" in _capi.last_error()
+    with pytest.raises(ValueError):
+        _capi.check(rc, "sas_range_rows")
+
+
+def test_select_rows_gpu_weights_and_size():
+    """select_rows(device=...) returns the reference's selector fields: s = ceil(oversample * width) rows drawn with
+    replacement, weights 1 / sqrt(s pi_i), strategy and anchors carried over."""
+    rng = np.random.default_rng(3)
+    b = rng.standard_normal((4000, 9))
+    rhs = b @ rng.standard_normal(9) + 1e-3 * rng.standard_normal(4000)
+    sel = offline.select_rows(b, rhs, strategy="leverage", oversample=4.0, seed=7, anchors=(0.5,),
+                              device=torch.device("cuda:0"))
+    ref = offline.select_rows(b, rhs, strategy="leverage", oversample=4.0, seed=7, anchors=(0.5,))
+    assert sel.size == ref.size == 40 and sel.strategy == "leverage" and sel.anchors == (0.5,)
+    assert np.array_equal(sel.indices, ref.indices)
+    np.testing.assert_allclose(sel.weights, ref.weights, rtol=1e-9)
