@@ -380,51 +380,81 @@ __global__ void __launch_bounds__(256, 2) k_resid_stencil_blk(const double* __re
 // operations per edge coefficient instead of 10 + DP + 4.  Same partials.
 // (Neighbour indices two nodes ahead + L2 prefetches of the next node's blocks: measured
 // slower, 0.208 vs 0.195 s on config 5 - profiles/r02e/r02e_resid_pf.jsonl.)
-template <int E, int DP>
-__global__ void __launch_bounds__(256, 2) k_resid_stencil_w(const double* __restrict__ x, int64_t n, int64_t P,
-                                                            const int32_t* __restrict__ nbr,
-                                                            const double* __restrict__ phi, double hh,
-                                                            const double* __restrict__ b,
-                                                            const double* __restrict__ params,
-                                                            double* __restrict__ part) {
-  static_assert(kResidPB == 64, "one warp = 64 parameter values");
+#ifndef SAS_RESID_PPL
+#define SAS_RESID_PPL 2
+#endif
+// PPL = parameter values per lane: 2 (one warp per node) or 1 (two warps per node, 32
+// parameter values each: half the registers per thread, three resident CTAs).
+template <int E, int DP, int PPL = SAS_RESID_PPL>
+__global__ void __launch_bounds__(256, PPL == 2 ? 2 : 3) k_resid_stencil_w(const double* __restrict__ x, int64_t n,
+                                                                          int64_t P, const int32_t* __restrict__ nbr,
+                                                                          const double* __restrict__ phi, double hh,
+                                                                          const double* __restrict__ b,
+                                                                          const double* __restrict__ params,
+                                                                          double* __restrict__ part) {
+  static_assert(kResidPB == 64 && (PPL == 1 || PPL == 2), "a node's 64 parameter values = one or two warps");
+  constexpr int WPN = 2 / PPL;   // warps per node
+  constexpr int NPI = 8 / WPN;   // nodes per CTA pass
   __shared__ double red[32];
   __shared__ double tab_s[2048];
-  __shared__ double rsum[kResidPB][8];
-  __shared__ double asum[kResidPB][8];
+  __shared__ double rsum[kResidPB][NPI];
+  __shared__ double asum[kResidPB][NPI];
   for (int j = threadIdx.x; j < 2048; j += blockDim.x) tab_s[j] = g_exp2_tab2048[j];
   __syncthreads();
   const double inv_hh = 1.0 / hh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wn = warp / WPN;                          // node slot of this warp
+  const int q0 = (warp % WPN) * 32 + PPL * lane;      // first parameter value of this lane in the block
   const int64_t pb = (int64_t)blockIdx.y * kResidPB;
   const int npb = (int)((P - pb) < kResidPB ? (P - pb) : kResidPB);
-  double pu[2][DP];
+  double pu[PPL][DP];
 #pragma unroll
-  for (int u = 0; u < 2; ++u)
+  for (int u = 0; u < PPL; ++u)
 #pragma unroll
-    for (int k = 0; k < DP; ++k)
-      pu[u][k] = (2 * lane + u < npb) ? params[(pb + 2 * lane + u) * DP + k] * SAS_INVLN2X2K : 0.0;
-  const double2* xb = reinterpret_cast<const double2*>(x + (int64_t)blockIdx.y * n * kResidPB) + lane;
-  double rr[2] = {0.0, 0.0}, aa[2] = {0.0, 0.0}, bb = 0.0;
-  const int64_t nstride = (int64_t)gridDim.x * 8;
-  for (int64_t i = (int64_t)blockIdx.x * 8 + warp; i < n; i += nstride) {
+    for (int k = 0; k < DP; ++k) pu[u][k] = (q0 + u < npb) ? params[(pb + q0 + u) * DP + k] * SAS_INVLN2X2K : 0.0;
+  const double* xb = x + (int64_t)blockIdx.y * n * kResidPB + q0;
+  auto ldx = [&](int64_t node, double (&v)[PPL]) {
+    if constexpr (PPL == 2) {
+      const double2 t = __ldg(reinterpret_cast<const double2*>(xb + node * kResidPB));
+      v[0] = t.x;
+      v[1] = t.y;
+    } else {
+      v[0] = __ldg(xb + node * kResidPB);
+    }
+  };
+  double rr[PPL], aa[PPL], bb = 0.0;
+#pragma unroll
+  for (int u = 0; u < PPL; ++u) rr[u] = aa[u] = 0.0;
+  const int64_t nstride = (int64_t)gridDim.x * NPI;
+  for (int64_t i = (int64_t)blockIdx.x * NPI + wn; i < n; i += nstride) {
     int m[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) m[e] = __ldg(nbr + i * E + e);
-    const double2 xi = __ldg(xb + i * (kResidPB / 2));
-    double2 xm[E];
+    double xi[PPL], xm[E][PPL];
+    ldx(i, xi);
 #pragma unroll
-    for (int e = 0; e < E; ++e) xm[e] = (m[e] >= 0) ? __ldg(xb + (int64_t)m[e] * (kResidPB / 2)) : make_double2(0.0, 0.0);
+    for (int e = 0; e < E; ++e) {
+      if (m[e] >= 0) {
+        ldx(m[e], xm[e]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < PPL; ++u) xm[e][u] = 0.0;
+      }
+    }
     const double bi = __ldg(b + i);
-    double acc[2] = {0.0, 0.0}, ab[2] = {0.0, 0.0};
-    const double axi[2] = {fabs(xi.x), fabs(xi.y)};
+    double acc[PPL], ab[PPL], axi[PPL];
+#pragma unroll
+    for (int u = 0; u < PPL; ++u) {
+      acc[u] = ab[u] = 0.0;
+      axi[u] = fabs(xi[u]);
+    }
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       double phv[DP];
 #pragma unroll
       for (int k = 0; k < DP; ++k) phv[k] = __ldg(phi + (i * E + e) * DP + k);
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < PPL; ++u) {
         double arg = pu[u][0] * phv[0];
 #pragma unroll
         for (int k = 1; k < DP; ++k) arg = fma(pu[u][k], phv[k], arg);
@@ -439,13 +469,12 @@ __global__ void __launch_bounds__(256, 2) k_resid_stencil_w(const double* __rest
         const double res = fma(t, q, t);
         const int keep = (ki >= SAS_EXP2K_KMIN) ? -1 : 0;
         const double c = __hiloint2double((__double2hiint(res) + ((ki >> 11) << 20)) & keep, __double2loint(res) & keep);
-        const double xv = u ? xi.y : xi.x, xn = u ? xm[e].y : xm[e].x;
-        acc[u] = fma(c, xv - xn, acc[u]);
-        ab[u] = fma(c, axi[u] + fabs(xn), ab[u]);   // |A| |x|: c_e > 0
+        acc[u] = fma(c, xi[u] - xm[e][u], acc[u]);
+        ab[u] = fma(c, axi[u] + fabs(xm[e][u]), ab[u]);   // |A| |x|: c_e > 0
       }
     }
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < PPL; ++u) {
       const double res = fma(acc[u], inv_hh, -bi);
       const double av = ab[u] * inv_hh;
       rr[u] = fma(res, res, rr[u]);
@@ -454,14 +483,14 @@ __global__ void __launch_bounds__(256, 2) k_resid_stencil_w(const double* __rest
     bb = fma(bi, bi, bb);
   }
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {
-    rsum[2 * lane + u][warp] = rr[u];
-    asum[2 * lane + u][warp] = aa[u];
+  for (int u = 0; u < PPL; ++u) {
+    rsum[q0 + u][wn] = rr[u];
+    asum[q0 + u][wn] = aa[u];
   }
-  const double tbb = block_sum(lane == 0 ? bb : 0.0, red);  // (its __syncthreads also publishes rsum)
+  const double tbb = block_sum((lane == 0 && warp % WPN == 0) ? bb : 0.0, red);  // (its __syncthreads also publishes rsum)
   if (threadIdx.x < npb) {
     double t = 0.0, ta = 0.0;
-    for (int w = 0; w < 8; ++w) {
+    for (int w = 0; w < NPI; ++w) {
       t += rsum[threadIdx.x][w];
       ta += asum[threadIdx.x][w];
     }
