@@ -384,7 +384,8 @@ __global__ void __launch_bounds__(256, 2) k_resid_stencil_blk(const double* __re
 #define SAS_RESID_PPL 2
 #endif
 // PPL = parameter values per lane: 2 (one warp per node) or 1 (two warps per node, 32
-// parameter values each: half the registers per thread, three resident CTAs).
+// parameter values each: half the registers per thread, three resident CTAs - measured
+// slower, 0.331 vs 0.193 s on config 5: the broadcast loads per FP64 operation double).
 template <int E, int DP, int PPL = SAS_RESID_PPL>
 __global__ void __launch_bounds__(256, PPL == 2 ? 2 : 3) k_resid_stencil_w(const double* __restrict__ x, int64_t n,
                                                                           int64_t P, const int32_t* __restrict__ nbr,
