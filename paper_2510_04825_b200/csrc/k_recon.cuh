@@ -387,15 +387,16 @@ __global__ void __launch_bounds__(256, 2) k_resid_stencil_blk(const double* __re
 // parameter values each: half the registers per thread, three resident CTAs - measured
 // slower, 0.331 vs 0.193 s on config 5: the broadcast loads per FP64 operation double).
 template <int E, int DP, int PPL = SAS_RESID_PPL>
-__global__ void __launch_bounds__(256, PPL == 2 ? 2 : 3) k_resid_stencil_w(const double* __restrict__ x, int64_t n,
+__global__ void __launch_bounds__(256, PPL == 1 ? 3 : 2) k_resid_stencil_w(const double* __restrict__ x, int64_t n,
                                                                           int64_t P, const int32_t* __restrict__ nbr,
                                                                           const double* __restrict__ phi, double hh,
                                                                           const double* __restrict__ b,
                                                                           const double* __restrict__ params,
                                                                           double* __restrict__ part) {
-  static_assert(kResidPB == 64 && (PPL == 1 || PPL == 2), "a node's 64 parameter values = one or two warps");
-  constexpr int WPN = 2 / PPL;   // warps per node
-  constexpr int NPI = 8 / WPN;   // nodes per CTA pass
+  static_assert(kResidPB == 64 && (PPL == 1 || PPL == 2 || PPL == 4), "a node's 64 parameter values = 64 / PPL lanes");
+  static_assert((DP % 2) == 0, "phi rows are read as double2");
+  constexpr int LPN = kResidPB / PPL;   // lanes per node: 64 (two warps), 32, 16 (two nodes per warp)
+  constexpr int NPI = 256 / LPN;        // nodes per CTA pass
   __shared__ double red[32];
   __shared__ double tab_s[2048];
   __shared__ double rsum[kResidPB][NPI];
@@ -404,8 +405,8 @@ __global__ void __launch_bounds__(256, PPL == 2 ? 2 : 3) k_resid_stencil_w(const
   __syncthreads();
   const double inv_hh = 1.0 / hh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wn = warp / WPN;                          // node slot of this warp
-  const int q0 = (warp % WPN) * 32 + PPL * lane;      // first parameter value of this lane in the block
+  const int wn = threadIdx.x / LPN;                   // node slot of this lane
+  const int q0 = PPL * (threadIdx.x % LPN);           // first parameter value of this lane in the block
   const int64_t pb = (int64_t)blockIdx.y * kResidPB;
   const int npb = (int)((P - pb) < kResidPB ? (P - pb) : kResidPB);
   double pu[PPL][DP];
@@ -415,10 +416,13 @@ __global__ void __launch_bounds__(256, PPL == 2 ? 2 : 3) k_resid_stencil_w(const
     for (int k = 0; k < DP; ++k) pu[u][k] = (q0 + u < npb) ? params[(pb + q0 + u) * DP + k] * SAS_INVLN2X2K : 0.0;
   const double* xb = x + (int64_t)blockIdx.y * n * kResidPB + q0;
   auto ldx = [&](int64_t node, double (&v)[PPL]) {
-    if constexpr (PPL == 2) {
-      const double2 t = __ldg(reinterpret_cast<const double2*>(xb + node * kResidPB));
-      v[0] = t.x;
-      v[1] = t.y;
+    if constexpr (PPL >= 2) {
+#pragma unroll
+      for (int h = 0; h < PPL / 2; ++h) {
+        const double2 t = __ldg(reinterpret_cast<const double2*>(xb + node * kResidPB) + h);
+        v[2 * h] = t.x;
+        v[2 * h + 1] = t.y;
+      }
     } else {
       v[0] = __ldg(xb + node * kResidPB);
     }
@@ -453,7 +457,11 @@ __global__ void __launch_bounds__(256, PPL == 2 ? 2 : 3) k_resid_stencil_w(const
     for (int e = 0; e < E; ++e) {
       double phv[DP];
 #pragma unroll
-      for (int k = 0; k < DP; ++k) phv[k] = __ldg(phi + (i * E + e) * DP + k);
+      for (int k = 0; k < DP; k += 2) {   // rows of DP doubles, DP even: 16-byte aligned
+        const double2 t = __ldg(reinterpret_cast<const double2*>(phi + (i * E + e) * DP + k));
+        phv[k] = t.x;
+        phv[k + 1] = t.y;
+      }
 #pragma unroll
       for (int u = 0; u < PPL; ++u) {
         double arg = pu[u][0] * phv[0];
@@ -488,7 +496,7 @@ __global__ void __launch_bounds__(256, PPL == 2 ? 2 : 3) k_resid_stencil_w(const
     rsum[q0 + u][wn] = rr[u];
     asum[q0 + u][wn] = aa[u];
   }
-  const double tbb = block_sum((lane == 0 && warp % WPN == 0) ? bb : 0.0, red);  // (its __syncthreads also publishes rsum)
+  const double tbb = block_sum((threadIdx.x % LPN == 0) ? bb : 0.0, red);  // (its __syncthreads also publishes rsum)
   if (threadIdx.x < npb) {
     double t = 0.0, ta = 0.0;
     for (int w = 0; w < NPI; ++w) {
