@@ -42,38 +42,60 @@ __global__ void __launch_bounds__(256) k_lift_dmma(const double* __restrict__ X,
   const int kp = ((r + 3) / 4) * 4;
   double* Xs = lsm;                      // 64 x ld
   double* Cs = lsm + kLiftNodes * ld;    // 64 x ld
-  const int64_t i0 = (int64_t)blockIdx.x * kLiftNodes;
   const int64_t p0 = (int64_t)blockIdx.y * kLiftPar;
+  // the C^T tile once per CTA (the CTA walks node tiles blockIdx.x, + gridDim.x, ...); the
+  // K padding of both tiles is zeroed here and never written again
   for (int e = threadIdx.x; e < kLiftNodes * kp; e += blockDim.x) {
     const int row = e / kp, k = e - row * kp;
-    const int64_t i = i0 + row, p = p0 + row;
-    Xs[row * ld + k] = (i < n && k < r) ? X[i * r + k] : 0.0;
+    const int64_t p = p0 + row;
     Cs[row * ld + k] = (p < P && k < r) ? C[p * r + k] : 0.0;
+    Xs[row * ld + k] = 0.0;
   }
-  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double acc[8][2];
-#pragma unroll
-  for (int t = 0; t < 8; ++t) acc[t][0] = acc[t][1] = 0.0;
   const double* xa = Xs + (warp * 8 + (lane >> 2)) * ld + (lane & 3);
   const double* cb = Cs + (lane >> 2) * ld + (lane & 3);
-  for (int k0 = 0; k0 < kp; k0 += 4) {
-    const double a = xa[k0];
+  // element e of the contiguous 64 x r tile -> (row, k), stepped by 256 without a division per element
+  const int dq = 256 / r, dr = 256 - dq * r;
+  const int64_t ntiles = (n + kLiftNodes - 1) / kLiftNodes;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t i0 = tile * kLiftNodes;
+    const int nrow = (int)((n - i0 < kLiftNodes) ? (n - i0) : kLiftNodes);
+    __syncthreads();   // the previous tile's fragments are read; Cs is in
+    {
+      const double* src = X + i0 * r;
+      int row = threadIdx.x / r, k = threadIdx.x - row * r;
+      for (int e = threadIdx.x; e < kLiftNodes * r; e += 256) {
+        Xs[row * ld + k] = (row < nrow) ? src[e] : 0.0;
+        row += dq;
+        k += dr;
+        if (k >= r) {
+          k -= r;
+          ++row;
+        }
+      }
+    }
+    __syncthreads();
+    double acc[8][2];
 #pragma unroll
-    for (int t = 0; t < 8; ++t) dmma884_r(acc[t][0], acc[t][1], a, cb[t * 8 * ld + k0]);
-  }
-  const int64_t i = i0 + warp * 8 + (lane >> 2);
-  if (i < n) {
+    for (int t = 0; t < 8; ++t) acc[t][0] = acc[t][1] = 0.0;
+    for (int k0 = 0; k0 < kp; k0 += 4) {
+      const double a = xa[k0];
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const int64_t p = p0 + t * 8 + 2 * (lane & 3);
-      if (BLK16) {
-        constexpr int PB = SAS_RESID_PB;
-        if (p < P) x[((p / PB) * n + i) * PB + (p % PB)] = acc[t][0];
-        if (p + 1 < P) x[(((p + 1) / PB) * n + i) * PB + ((p + 1) % PB)] = acc[t][1];
-      } else {
-        if (p < P) x[p * n + i] = acc[t][0];
-        if (p + 1 < P) x[(p + 1) * n + i] = acc[t][1];
+      for (int t = 0; t < 8; ++t) dmma884_r(acc[t][0], acc[t][1], a, cb[t * 8 * ld + k0]);
+    }
+    const int64_t i = i0 + warp * 8 + (lane >> 2);
+    if (i < n) {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int64_t p = p0 + t * 8 + 2 * (lane & 3);
+        if (BLK16) {
+          constexpr int PB = SAS_RESID_PB;
+          if (p < P) x[((p / PB) * n + i) * PB + (p % PB)] = acc[t][0];
+          if (p + 1 < P) x[(((p + 1) / PB) * n + i) * PB + ((p + 1) % PB)] = acc[t][1];
+        } else {
+          if (p < P) x[p * n + i] = acc[t][0];
+          if (p + 1 < P) x[(p + 1) * n + i] = acc[t][1];
+        }
       }
     }
   }
@@ -389,6 +411,7 @@ __global__ void __launch_bounds__(256, 2) k_resid_stencil_blk(const double* __re
 template <int E, int DP, int PPL = SAS_RESID_PPL>
 __global__ void __launch_bounds__(256, PPL == 1 ? 3 : 2) k_resid_stencil_w(const double* __restrict__ x, int64_t n,
                                                                           int64_t P, const int32_t* __restrict__ nbr,
+                                                                          const int32_t* __restrict__ order,
                                                                           const double* __restrict__ phi, double hh,
                                                                           const double* __restrict__ b,
                                                                           const double* __restrict__ params,
@@ -431,10 +454,32 @@ __global__ void __launch_bounds__(256, PPL == 1 ? 3 : 2) k_resid_stencil_w(const
 #pragma unroll
   for (int u = 0; u < PPL; ++u) rr[u] = aa[u] = 0.0;
   const int64_t nstride = (int64_t)gridDim.x * NPI;
-  for (int64_t i = (int64_t)blockIdx.x * NPI + wn; i < n; i += nstride) {
+#ifdef SAS_RESID_NBR_AHEAD
+  // neighbour indices one node ahead (the nbr -> x block chain is the top stall of this kernel)
+  const int64_t j0 = (int64_t)blockIdx.x * NPI + wn;
+  int mn[E];
+  {
+    const int64_t i1 = (j0 < n) ? (order ? (int64_t)__ldg(order + j0) : j0) : 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) mn[e] = __ldg(nbr + i1 * E + e);
+  }
+#endif
+  for (int64_t j = (int64_t)blockIdx.x * NPI + wn; j < n; j += nstride) {
+    const int64_t i = order ? (int64_t)__ldg(order + j) : j;   // traversal order (a permutation of the nodes)
     int m[E];
+#ifdef SAS_RESID_NBR_AHEAD
+#pragma unroll
+    for (int e = 0; e < E; ++e) m[e] = mn[e];
+    {
+      const int64_t jn = (j + nstride < n) ? j + nstride : j;
+      const int64_t i1 = order ? (int64_t)__ldg(order + jn) : jn;
+#pragma unroll
+      for (int e = 0; e < E; ++e) mn[e] = __ldg(nbr + i1 * E + e);
+    }
+#else
 #pragma unroll
     for (int e = 0; e < E; ++e) m[e] = __ldg(nbr + i * E + e);
+#endif
     double xi[PPL], xm[E][PPL];
     ldx(i, xi);
 #pragma unroll

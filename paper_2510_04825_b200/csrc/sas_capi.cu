@@ -163,6 +163,7 @@ struct sas_plan {
   double* Xfrag = nullptr;  // K3 v3 fragment-ordered X^T
   // full operator for the residual checker
   int32_t* full_nbr = nullptr;  // n x E neighbours (int32: n < 2^31), -1 on Dirichlet edges
+  int32_t* resid_order = nullptr;  // K6 traversal order of the nodes (a permutation; null: index order)
   double* full_phi = nullptr;
   void* full_b = nullptr;
   std::vector<int64_t*> csr_rp, csr_ci;
@@ -295,7 +296,7 @@ static void plan_free(sas_plan* pl) {
   if (!pl) return;
   DevGuard g(pl->device);
   void* ptrs[] = {pl->X, pl->S, pl->w, pl->t, pl->proj, pl->kind, pl->scale, pl->rate, pl->blocks,
-                  pl->phi, pl->G, pl->gmap, pl->pts, pl->D, pl->Dfrag, pl->Xfrag, pl->full_nbr, pl->full_phi, pl->full_b,
+                  pl->phi, pl->G, pl->gmap, pl->pts, pl->D, pl->Dfrag, pl->Xfrag, pl->full_nbr, pl->resid_order, pl->full_phi, pl->full_b,
                   pl->csr_rp_d, pl->csr_ci_d, pl->csr_va_d, pl->Mscr, pl->cw_mg, pl->wy_mg, pl->wy_slots, pl->rpart, pl->xscr, pl->fco,
                   pl->h_params, pl->h_ctab, pl->h_rhs, pl->h_coef, pl->h_sres, pl->h_outv,
                   pl->h_status, pl->h_bad};
@@ -1304,7 +1305,9 @@ static int launch_lift_dmma(sas_plan* pl, const double* coef, int64_t P, double*
   if (int rc = smem_optin<k_lift_dmma<true>>(false)) return rc;
   for (int64_t p0 = 0; p0 < P; p0 += 65535LL * kLiftPar) {
     const int64_t pc = (P - p0 < 65535LL * kLiftPar) ? P - p0 : 65535LL * kLiftPar;
-    dim3 grid((unsigned)((pl->n + kLiftNodes - 1) / kLiftNodes), (unsigned)((pc + kLiftPar - 1) / kLiftPar));
+    // persistent over node tiles: 8 waves of CTAs per parameter tile at most (the C^T tile is loaded once per CTA)
+    const int64_t ntiles = (pl->n + kLiftNodes - 1) / kLiftNodes;
+    dim3 grid((unsigned)std::min<int64_t>(ntiles, (int64_t)pl->sms * 32), (unsigned)((pc + kLiftPar - 1) / kLiftPar));
     if (blk16)  // p0 is a multiple of kResidPB: the blocks of this launch start at block p0 / kResidPB
       k_lift_dmma<true><<<grid, 256, smem, st>>>((const double*)pl->X, pl->n, pl->r, coef + p0 * pl->r, pc,
                                                  x + p0 * pl->n);
@@ -1359,6 +1362,39 @@ extern "C" int sas_plan_set_operator(sas_plan* pl, const int64_t* const* row_ptr
       std::vector<int32_t> nb32((size_t)pl->n * pl->E);
       for (size_t q = 0; q < nb32.size(); ++q) nb32[q] = (int32_t)nbr_full[q];
       if ((rc = dupload(&pl->full_nbr, nb32.data(), nb32.size() * sizeof(int32_t)))) return rc;
+      // K6 traversal order.  On a g^3 lattice numbered x fastest (neighbour strides 1, g, g^2,
+      // read off an interior node) the checker sweeps y-strips of whole z columns, so that a
+      // node's x block is still in L2 when it comes back as the -z / +z neighbour (index order
+      // spreads those three uses over 2 g^2 nodes = 76 MB of traffic at g = 216 and reads x twice
+      // from HBM).  Any permutation gives the same sums up to their order; other graphs keep index order.
+      if (pl->resid_order) { cudaFree(pl->resid_order); pl->resid_order = nullptr; }
+      // Measured (profiles/r02e/r02e_resid_order2.jsonl): HBM reads per 64-parameter pass 16.3 -> 13.1 GB, but the
+      // extra dependent index load costs more than the L2 hits save (0.193 vs 0.181 s): opt-in only.
+      static const bool strips = getenv("SAS_RESID_ORDER") && !strcmp(getenv("SAS_RESID_ORDER"), "strips");
+      if (pl->E == 6 && strips) {
+        const int64_t n = pl->n;
+        int64_t i0 = n / 2;   // an interior node (all six neighbours present) near the middle
+        for (int t = 0; t < 4096 && i0 < n; ++t, i0 += 997) {
+          bool all = true;
+          for (int e = 0; e < 6; ++e) all = all && nb32[(size_t)i0 * 6 + e] >= 0;
+          if (all) break;
+        }
+        if (i0 >= n) i0 = n / 2;
+        int64_t st[6];
+        for (int e = 0; e < 6; ++e) st[e] = nb32[(size_t)i0 * 6 + e] < 0 ? 0 : std::llabs((long long)nb32[(size_t)i0 * 6 + e] - i0);
+        std::sort(st, st + 6);
+        const int64_t g1 = st[2], g2 = st[4];
+        if (st[0] == 1 && st[1] == 1 && g1 == st[3] && g2 == st[5] && g1 > 1 && g2 == g1 * g1 && n == g2 * g1 && g1 >= 64) {
+          const int64_t H = 48;   // strip height: 3 uses of a block within 2 H g nodes (17 MB of x + phi at g = 216), 2 / H halo rows
+          std::vector<int32_t> ord((size_t)n);
+          size_t q = 0;
+          for (int64_t y0 = 0; y0 < g1; y0 += H)
+            for (int64_t z = 0; z < g1; ++z)
+              for (int64_t y = y0; y < std::min(y0 + H, g1); ++y)
+                for (int64_t x = 0; x < g1; ++x) ord[q++] = (int32_t)(z * g2 + y * g1 + x);
+          if ((rc = dupload(&pl->resid_order, ord.data(), ord.size() * sizeof(int32_t)))) return rc;
+        }
+      }
     }
     if ((rc = dupload(&pl->full_phi, phi_full, (size_t)pl->n * pl->E * pl->dp * sizeof(double)))) return rc;
   } else if (pl->op == SAS_OP_AFFINE) {
@@ -1429,11 +1465,11 @@ extern "C" int sas_residual(sas_plan* pl, const void* params, const void* coef, 
       dim3 g2(nb, (unsigned)((pc + kResidPB - 1) / kResidPB));
       static const bool generic = getenv("SAS_RESID_GENERIC") != nullptr;   // A/B: the per-edge kernel
       if (!generic && pl->E == 6 && pl->dp == 6)
-        k_resid_stencil_w<6, 6><<<g2, 256, 0, st>>>(pl->xscr, pl->n, pc, pl->full_nbr, pl->full_phi, pl->hh,
+        k_resid_stencil_w<6, 6><<<g2, 256, 0, st>>>(pl->xscr, pl->n, pc, pl->full_nbr, pl->resid_order, pl->full_phi, pl->hh,
                                                     (const double*)pl->full_b, (const double*)params + p0 * pl->dp,
                                                     pl->rpart + p0 * nb * 3);
       else if (!generic && pl->E == 4 && pl->dp == 4)
-        k_resid_stencil_w<4, 4><<<g2, 256, 0, st>>>(pl->xscr, pl->n, pc, pl->full_nbr, pl->full_phi, pl->hh,
+        k_resid_stencil_w<4, 4><<<g2, 256, 0, st>>>(pl->xscr, pl->n, pc, pl->full_nbr, pl->resid_order, pl->full_phi, pl->hh,
                                                     (const double*)pl->full_b, (const double*)params + p0 * pl->dp,
                                                     pl->rpart + p0 * nb * 3);
       else
