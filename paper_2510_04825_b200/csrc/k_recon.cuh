@@ -454,8 +454,8 @@ __global__ void __launch_bounds__(256, PPL == 1 ? 3 : 2) k_resid_stencil_w(const
 #pragma unroll
   for (int u = 0; u < PPL; ++u) rr[u] = aa[u] = 0.0;
   const int64_t nstride = (int64_t)gridDim.x * NPI;
-#ifdef SAS_RESID_NBR_AHEAD
-  // neighbour indices one node ahead (the nbr -> x block chain is the top stall of this kernel)
+  // neighbour indices one node ahead (the nbr -> x block chain is the top stall of this kernel:
+  // config 5 0.181 -> 0.177 s, config 3 15.1 -> 14.0 ms)
   const int64_t j0 = (int64_t)blockIdx.x * NPI + wn;
   int mn[E];
   {
@@ -467,7 +467,6 @@ __global__ void __launch_bounds__(256, PPL == 1 ? 3 : 2) k_resid_stencil_w(const
   for (int64_t j = (int64_t)blockIdx.x * NPI + wn; j < n; j += nstride) {
     const int64_t i = order ? (int64_t)__ldg(order + j) : j;   // traversal order (a permutation of the nodes)
     int m[E];
-#ifdef SAS_RESID_NBR_AHEAD
 #pragma unroll
     for (int e = 0; e < E; ++e) m[e] = mn[e];
     {
@@ -476,10 +475,6 @@ __global__ void __launch_bounds__(256, PPL == 1 ? 3 : 2) k_resid_stencil_w(const
 #pragma unroll
       for (int e = 0; e < E; ++e) mn[e] = __ldg(nbr + i1 * E + e);
     }
-#else
-#pragma unroll
-    for (int e = 0; e < E; ++e) m[e] = __ldg(nbr + i * E + e);
-#endif
     double xi[PPL], xm[E][PPL];
     ldx(i, xi);
 #pragma unroll
