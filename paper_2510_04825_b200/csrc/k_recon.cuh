@@ -463,7 +463,6 @@ __global__ void __launch_bounds__(256, PPL == 1 ? 3 : 2) k_resid_stencil_w(const
 #pragma unroll
     for (int e = 0; e < E; ++e) mn[e] = __ldg(nbr + i1 * E + e);
   }
-#endif
   for (int64_t j = (int64_t)blockIdx.x * NPI + wn; j < n; j += nstride) {
     const int64_t i = order ? (int64_t)__ldg(order + j) : j;   // traversal order (a permutation of the nodes)
     int m[E];
