@@ -184,3 +184,29 @@ def test_estimate_residual_formula():
     plan2 = dataclasses.replace(plan, selector=unweighted)
     with pytest.raises(ValueError):
         online.estimate_residual(plan2, sol)
+
+
+def test_precompute_spot_check_raises_on_inconsistent_blocks():
+    """The reference's plan check (online.py:86-96): affine blocks that disagree with the
+    system's row oracle at basis.points[0] by more than 1e-10 raise RankDeficiencyError
+    (before any device plan is built); consistent ones pass the same check."""
+    from paper_2510_04825_b200.errors import RankDeficiencyError
+    case = load("tridiag_lupp")
+    system, basis, sel = case.system, case.basis, case.selector
+    idx = np.asarray(sel.indices, dtype=np.int64)
+    uniq, inverse = np.unique(idx, return_inverse=True)
+    blocks = tuple(online._rows_times_basis(t.matrix[uniq], basis.basis)[inverse] for t in system.affine_terms)
+    online._spot_check(system, basis, idx, uniq, inverse, blocks)          # consistent: no error
+
+    class Skewed:
+        """Same affine terms, but a row oracle that is off by 1e-6 relative."""
+        def __init__(self, inner):
+            self._inner = inner
+        def __getattr__(self, name):
+            return getattr(self._inner, name)
+        def rows(self, p, rows):
+            m = sp.csr_matrix(self._inner.matrix(p))[np.asarray(rows)]
+            return m * (1.0 + 1e-6)
+
+    with pytest.raises(RankDeficiencyError, match="disagree with row oracle"):
+        online.precompute_online(Skewed(system), basis, sel)
