@@ -408,7 +408,9 @@ __global__ void __launch_bounds__(256, 2) k_resid_stencil_blk(const double* __re
 // PPL = parameter values per lane: 2 (one warp per node) or 1 (two warps per node, 32
 // parameter values each: half the registers per thread, three resident CTAs - measured
 // slower, 0.331 vs 0.193 s on config 5: the broadcast loads per FP64 operation double).
-template <int E, int DP, int PPL = SAS_RESID_PPL>
+// FLOOR = false: the caller did not ask for the rounding floor; || |A| |x| || is skipped
+// (2 of the DP + 11 FP64 operations per edge coefficient) and its partial is written as 0.
+template <int E, int DP, bool FLOOR = true, int PPL = SAS_RESID_PPL>
 __global__ void __launch_bounds__(256, PPL == 1 ? 3 : 2) k_resid_stencil_w(const double* __restrict__ x, int64_t n,
                                                                           int64_t P, const int32_t* __restrict__ nbr,
                                                                           const int32_t* __restrict__ order,
@@ -518,15 +520,17 @@ __global__ void __launch_bounds__(256, PPL == 1 ? 3 : 2) k_resid_stencil_w(const
         const int keep = (ki >= SAS_EXP2K_KMIN) ? -1 : 0;
         const double c = __hiloint2double((__double2hiint(res) + ((ki >> 11) << 20)) & keep, __double2loint(res) & keep);
         acc[u] = fma(c, xi[u] - xm[e][u], acc[u]);
-        ab[u] = fma(c, axi[u] + fabs(xm[e][u]), ab[u]);   // |A| |x|: c_e > 0
+        if constexpr (FLOOR) ab[u] = fma(c, axi[u] + fabs(xm[e][u]), ab[u]);   // |A| |x|: c_e > 0
       }
     }
 #pragma unroll
     for (int u = 0; u < PPL; ++u) {
       const double res = fma(acc[u], inv_hh, -bi);
-      const double av = ab[u] * inv_hh;
       rr[u] = fma(res, res, rr[u]);
-      aa[u] = fma(av, av, aa[u]);
+      if constexpr (FLOOR) {
+        const double av = ab[u] * inv_hh;
+        aa[u] = fma(av, av, aa[u]);
+      }
     }
     bb = fma(bi, bi, bb);
   }

@@ -1465,13 +1465,13 @@ extern "C" int sas_residual(sas_plan* pl, const void* params, const void* coef, 
       dim3 g2(nb, (unsigned)((pc + kResidPB - 1) / kResidPB));
       static const bool generic = getenv("SAS_RESID_GENERIC") != nullptr;   // A/B: the per-edge kernel
       if (!generic && pl->E == 6 && pl->dp == 6)
-        k_resid_stencil_w<6, 6><<<g2, 256, 0, st>>>(pl->xscr, pl->n, pc, pl->full_nbr, pl->resid_order, pl->full_phi, pl->hh,
-                                                    (const double*)pl->full_b, (const double*)params + p0 * pl->dp,
-                                                    pl->rpart + p0 * nb * 3);
+        (floor_est ? k_resid_stencil_w<6, 6, true> : k_resid_stencil_w<6, 6, false>)<<<g2, 256, 0, st>>>(
+            pl->xscr, pl->n, pc, pl->full_nbr, pl->resid_order, pl->full_phi, pl->hh, (const double*)pl->full_b,
+            (const double*)params + p0 * pl->dp, pl->rpart + p0 * nb * 3);
       else if (!generic && pl->E == 4 && pl->dp == 4)
-        k_resid_stencil_w<4, 4><<<g2, 256, 0, st>>>(pl->xscr, pl->n, pc, pl->full_nbr, pl->resid_order, pl->full_phi, pl->hh,
-                                                    (const double*)pl->full_b, (const double*)params + p0 * pl->dp,
-                                                    pl->rpart + p0 * nb * 3);
+        (floor_est ? k_resid_stencil_w<4, 4, true> : k_resid_stencil_w<4, 4, false>)<<<g2, 256, 0, st>>>(
+            pl->xscr, pl->n, pc, pl->full_nbr, pl->resid_order, pl->full_phi, pl->hh, (const double*)pl->full_b,
+            (const double*)params + p0 * pl->dp, pl->rpart + p0 * nb * 3);
       else
         k_resid_stencil_blk<<<g2, 256, 0, st>>>(pl->xscr, pl->n, pc, pl->full_nbr, pl->full_phi, pl->E, pl->dp,
                                                 pl->hh, (const double*)pl->full_b,

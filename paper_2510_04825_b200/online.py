@@ -715,7 +715,7 @@ def relative_residual(plan: OnlinePlan, parameters, coefficients, return_floor: 
         rows = np.stack([np.asarray(plan.system.full_rhs(p)) for p in parameters]).astype(g.np_dtype)
         b_t = torch.from_numpy(np.ascontiguousarray(rows)).to(dev)
     out = torch.empty(len(parameters), dtype=torch.float64, device=dev)
-    fl = torch.empty(len(parameters), dtype=torch.float64, device=dev)
+    fl = torch.empty(len(parameters), dtype=torch.float64, device=dev) if return_floor else None   # NULL: not computed
     st = torch.cuda.current_stream(g.device)
     _capi.check(g.lib.sas_residual(g.handle, _capi.ptr(pt), _capi.ptr(ct), len(parameters), _capi.ptr(tab_t),
                                    _capi.ptr(b_t), _capi.ptr(out), _capi.ptr(fl), C.c_void_p(st.cuda_stream)),
